@@ -1,0 +1,224 @@
+/*
+ * mdr.h — C-ABI of the B200 scoring / reduction / ADADELTA / LGA hot path.
+ *
+ * This is the drop-in boundary for the reference's operator API (namespace
+ * `mdreduce`, /root/reference/proj/include/mdreduce/<name>.hpp).  The reference has
+ * no C-ABI of its own; each entry point below names the C++ function it
+ * replaces.  The C++ header `include/mdreduce_b200.hpp` re-exposes these as the
+ * reference's exact C++ signatures (same structs, same exception types), so a
+ * reference caller recompiles unchanged.
+ *
+ * Conventions
+ *  - plain pointers + explicit counts, no torch / CUDA types in signatures;
+ *  - every call returns an int status (MDR_OK == 0); a failing call performs
+ *    no work (validation happens before any launch), mirroring the reference
+ *    throwing before work (SURVEY §8b "Errors");
+ *  - `*_batch` calls take HOST buffers and do H2D, kernels and D2H inside;
+ *    `*_dev` calls take DEVICE pointers, enqueue on the context stream and
+ *    return without synchronising (the resident-input path the bench times);
+ *  - one context per device; calls on one context are serialised.
+ */
+#ifndef MDR_H
+#define MDR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (exception taxonomy of errors.hpp:10-42) ------------- */
+enum {
+  MDR_OK = 0,
+  MDR_ERR_SIZE = 1,           /* SizeError                errors.hpp:10-13 */
+  MDR_ERR_BLOCK_SIZE = 2,     /* UnsupportedBlockSizeError errors.hpp:16-20 */
+  MDR_ERR_NUMERIC_DOMAIN = 3, /* NumericDomainError        errors.hpp:23-26 */
+  MDR_ERR_PARSE = 4,          /* ParseError                errors.hpp:29-42 */
+  MDR_ERR_CUDA = 5,           /* device / driver failure (new)           */
+  MDR_ERR_INVALID = 6         /* null pointer, bad enum (new)            */
+};
+
+/* ---- enums (reduce.hpp:13, mma.hpp:13-14) ------------------------------ */
+enum {
+  MDR_METHOD_BASELINE = 0,  /* ReduceMethod::Baseline: fp32 shuffle trees  */
+  MDR_METHOD_TCU = 1,       /* ReduceMethod::Tcu: paper's f16 MMA (compat) */
+  MDR_METHOD_TCU_SPLIT = 2  /* new: tf32 hi/lo error-compensated MMA       */
+};
+enum { MDR_ACCUM_HALF = 0, MDR_ACCUM_SINGLE = 1 };
+enum { MDR_LAYOUT_ROW = 0, MDR_LAYOUT_COL = 1 };
+/* pair-term arithmetic of the scoring kernel: FP64 reproduces the
+ * reference's double evaluate_atoms (docking.cpp:95-128) bit for bit;
+ * FP32 is the fast mode (tolerance parity only). */
+enum { MDR_PAIR_FP64 = 0, MDR_PAIR_FP32 = 1 };
+
+/* ---- plain-data structs ------------------------------------------------ */
+/* SyncStats reduce.hpp:33-54 (field order preserved). */
+typedef struct mdr_sync_stats {
+  uint64_t block_syncs;
+  uint64_t warp_shuffles;
+  uint64_t atomic_adds;
+  uint64_t memory_fences;
+  uint64_t mma_ops;
+  uint64_t shared_mem_bytes;
+  uint64_t precision_conversions;
+} mdr_sync_stats;
+
+/* LigandInstance instance_io.hpp:13-30, flattened (caller-owned). */
+typedef struct mdr_instance {
+  int32_t n_atoms;
+  int32_t n_sites;
+  int32_t n_rot;
+  int32_t reserved;
+  const double* atom_xyzw;     /* n_atoms x {x, y, z, weight}            */
+  const int32_t* atom_torsion; /* n_atoms, -1 = rigid                    */
+  const double* site_xyzdd;    /* n_sites x {x, y, z, depth, d0}         */
+} mdr_instance;
+
+/* LgaSettings docking.hpp:106-115 (same defaults via mdr_lga_defaults). */
+typedef struct mdr_lga_settings {
+  int32_t population_size;
+  int32_t generations;
+  int64_t max_evaluations;
+  double ls_fraction;
+  int32_t ls_max_iters;
+  int32_t partition;
+  double ls_convergence_tol;
+  double mutation_sigma;
+} mdr_lga_settings;
+
+/* LsRunRecord docking.hpp:117-123. */
+typedef struct mdr_ls_record {
+  double best_energy;
+  int32_t iterations;
+  int32_t converged;
+} mdr_ls_record;
+
+typedef struct mdr_ctx mdr_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+mdr_ctx* mdr_ctx_create(int device);
+void mdr_ctx_destroy(mdr_ctx* ctx);
+/* Use an external cudaStream_t (passed as void*); NULL restores the
+ * context's own stream. */
+int mdr_ctx_set_stream(mdr_ctx* ctx, void* cuda_stream);
+void* mdr_ctx_stream(mdr_ctx* ctx);
+int mdr_ctx_set_pair_precision(mdr_ctx* ctx, int pair_precision);
+/* Message of the last failing call on this context (thread-local copy). */
+const char* mdr_last_error(mdr_ctx* ctx);
+/* Number of kernel launches this context has enqueued so far. */
+uint64_t mdr_ctx_launch_count(mdr_ctx* ctx);
+int mdr_ctx_synchronize(mdr_ctx* ctx);
+const char* mdr_version(void);
+
+/* ---- L0 numeric units (half.hpp, mma.hpp) ------------------------------ */
+/* f32_to_half half.cpp:8-54 / half_to_f32 half.cpp:56-74, on the device
+ * (cvt.rn.f16.f32, subnormals kept). */
+int mdr_f32_to_half_batch(mdr_ctx* ctx, const float* in, size_t n, uint16_t* out);
+int mdr_half_to_f32_batch(mdr_ctx* ctx, const uint16_t* in, size_t n, float* out);
+/* mma mma.cpp:41-64 on tensor cores: n_tiles independent 16x16x16 tiles,
+ * a/b row-major binary16 (256 each), c/d row-major fp32 (256 each).
+ * accum == HALF rounds d to binary16 once (Accum16 Half mode). */
+int mdr_mma_batch(mdr_ctx* ctx, const uint16_t* a, const uint16_t* b,
+                  const float* c, int n_tiles, int accum, float* d);
+
+/* ---- L1 block reductions (reduce.hpp) ---------------------------------- */
+/* reduce4 reduce.cpp:80-111.  n_red reductions of n float4 {x,y,z,e}.
+ * method TCU: reference-compatible f16 MMA with AccumMode semantics;
+ * method TCU_SPLIT: tf32 hi/lo MMA, fp32-accurate;
+ * method BASELINE: simulate_block baseline (4 x baseline_block_reduce,
+ *   simblock.cpp:447-462; n must be a legal block size).
+ * stats = SyncStats of ONE reduction as the reference counts it. */
+int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red,
+                      int method, int accum, float* out, mdr_sync_stats* stats);
+/* baseline_block_reduce reduce.cpp:136-163, n_red blocks of `threads`. */
+int mdr_block_reduce_batch(mdr_ctx* ctx, const float* values, int threads,
+                           int n_red, float* out, mdr_sync_stats* stats);
+/* baseline_warp_reduce reduce.cpp:113-134, n_red warps of 32 lanes. */
+int mdr_warp_reduce_batch(mdr_ctx* ctx, const float* lanes, int n_red,
+                          float* out, mdr_sync_stats* stats);
+/* reduce7 reduce.cpp:165-209.  recs: n_red x n x {e,gx,gy,gz,tx,ty,tz}. */
+int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red,
+                      int method, int accum, float* out, mdr_sync_stats* stats);
+
+/* ---- L2 scoring (docking.hpp:44-63) ------------------------------------ */
+/* score docking.cpp:191-233 for n genotypes (n x dim, dim = 6 + n_rot,
+ * order x,y,z,phi,theta,alpha,torsions).  gradient n x dim, torque n x 3.
+ * stats = SyncStats of ONE score call. */
+int mdr_score_batch(mdr_ctx* ctx, const mdr_instance* inst,
+                    const double* genotypes, int n, int method, int accum,
+                    int partition, float* energy, float* gradient,
+                    float* torque, mdr_sync_stats* stats);
+/* score_reference docking.cpp:235-270 (double sums, exact per-group torsion
+ * torque). */
+int mdr_score_reference_batch(mdr_ctx* ctx, const mdr_instance* inst,
+                              const double* genotypes, int n, double* energy,
+                              double* gradient, double* torque);
+
+/* ---- L3 search drivers ------------------------------------------------- */
+/* adadelta_step docking.cpp:281-308 for n independent states (n x dim
+ * each).  Updates avg_sq_grad / avg_sq_update / genotype in place. */
+int mdr_adadelta_step_batch(mdr_ctx* ctx, int dim, int n, double rho,
+                            double epsilon, double* avg_sq_grad,
+                            double* avg_sq_update, double* genotype,
+                            const double* grad);
+/* local_search docking.cpp:310-351 for n starts, one device-resident
+ * ADADELTA loop per start.  stats = accumulated SyncStats per search. */
+int mdr_local_search_batch(mdr_ctx* ctx, const mdr_instance* inst,
+                           const double* starts, int n, int max_iters,
+                           double convergence_tol, int method, int accum,
+                           int partition, double* out_genotype,
+                           double* out_energy, int32_t* out_iterations,
+                           int32_t* out_converged, mdr_sync_stats* stats);
+
+/* lga_run docking.cpp:392-517 for n_runs independent seeds.
+ * best_genotype n_runs x dim; records n_runs x mdr_lga_max_records(s);
+ * n_records[i] valid records of run i; total_stats per run. */
+void mdr_lga_defaults(mdr_lga_settings* s);
+int mdr_lga_max_records(const mdr_lga_settings* s);
+int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method,
+                      int accum, const mdr_lga_settings* settings,
+                      const uint64_t* seeds, int n_runs, double* best_energy,
+                      double* best_genotype, int64_t* evaluations,
+                      int32_t* converged, int32_t* n_records,
+                      mdr_ls_record* records, mdr_sync_stats* total_stats);
+
+/* ---- resident-input (device pointer) variants -------------------------- */
+/* A device-resident ligand: uploaded once, reused by every _dev call. */
+typedef struct mdr_dev_instance mdr_dev_instance;
+mdr_dev_instance* mdr_instance_upload(mdr_ctx* ctx, const mdr_instance* inst);
+void mdr_instance_free(mdr_ctx* ctx, mdr_dev_instance* dinst);
+
+int mdr_score_dev(mdr_ctx* ctx, const mdr_dev_instance* dinst,
+                  const double* d_genotypes, int n, int method, int accum,
+                  int partition, float* d_energy, float* d_gradient,
+                  float* d_torque);
+int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* dinst,
+                         const double* d_starts, int n, int max_iters,
+                         double convergence_tol, int method, int accum,
+                         int partition, double* d_out_genotype,
+                         double* d_out_energy, int32_t* d_out_iterations,
+                         int32_t* d_out_converged, int32_t* d_status);
+
+/* LGA batch with all state on the device.  d_seeds: n_runs uint64 on the
+ * device.  Results stay on the device in an opaque batch object; read them
+ * with mdr_lga_batch_download.  The whole docking is one CUDA graph. */
+typedef struct mdr_lga_batch mdr_lga_batch;
+mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* dinst,
+                                    int method, int accum,
+                                    const mdr_lga_settings* settings,
+                                    int n_runs);
+void mdr_lga_batch_destroy(mdr_ctx* ctx, mdr_lga_batch* b);
+int mdr_lga_batch_run_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds);
+int mdr_lga_batch_download(mdr_ctx* ctx, mdr_lga_batch* b, double* best_energy,
+                           double* best_genotype, int64_t* evaluations,
+                           int32_t* converged, int32_t* n_records,
+                           mdr_ls_record* records, mdr_sync_stats* total_stats);
+/* Sum of evaluations over the batch's runs, reduced on the device into a
+ * single int64 at d_total (for D2H of one word per step). */
+int mdr_lga_batch_total_evals_dev(mdr_ctx* ctx, mdr_lga_batch* b, int64_t* d_total);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDR_H */
