@@ -1,0 +1,458 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 docking hot path (BASELINE.json metric
+"score+gradient evals/sec").
+
+Workload (SURVEY §8d, config C3 = BASELINE.json configs[2], the 1xB200 docking
+config): a synthetic small ligand — 20 atoms, 5 torsions, 64 receptor sites,
+built with the reference's random_instance recipe (tests/test_docking.cpp:39-59)
+from derive_rng(12345, "synth/small") — docked with 100 independent LGA runs
+(default LgaSettings, docking.hpp:106-115), ~2.8M score+gradient evaluations
+per step.  A step is one full docking of that ligand.  Multi-GPU: each rank
+docks its own 100 seeds (weak scaling, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+value    : device-resident (instance + seeds in HBM, CUDA graph of the whole
+           docking) evals/s, CUDA events on the launching stream, L2 flushed
+           before every timed step, max over ranks.
+e2e      : the same docking through the reference-facing host call
+           mdr_lga_run_batch (host buffers; upload, graph build, run, download).
+roofline : the dominant kernel (lga_ls_kernel, the device ADADELTA chain)
+           against the FP64 pipe (peak measured live by a DFMA kernel, see
+           DESIGN.md §6).
+cpu_baseline : the reference library itself (oracle/_ref, compiled in place
+           from /root/reference) timed on this host, one process per core.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2410_10447_b200._abi import (  # noqa: E402
+    BASELINE,
+    HALF,
+    PAIR_FP32,
+    PAIR_FP64,
+    SINGLE,
+    TCU,
+    TCU_SPLIT,
+    LgaSettings,
+    LsRecord,
+    SyncStats,
+    derive_rng,
+    random_instance,
+)
+
+METRIC = "score+gradient evals/sec"
+UNIT = "evals/s"
+N_ATOMS, N_ROT, N_SITES, N_RUNS = 20, 5, 64, 100
+METHODS = {"baseline": BASELINE, "tcu": TCU, "split": TCU_SPLIT}
+
+
+def workload():
+    inst = random_instance(derive_rng(12345, "synth/small"), N_ROT, N_ATOMS, N_SITES)
+    inst.name = "synth/small"
+    return inst
+
+
+def flop_per_eval(inst, partition):
+    """SURVEY §8d FLOP/eval (div = 1 flop; trig listed separately)."""
+    n_tors_atoms = int((inst.torsion >= 0).sum())
+    return (32 * inst.n_atoms * inst.n_sites + 30 * inst.n_atoms + 31 * n_tors_atoms + 165 + 25 * inst.n_rot
+            + 7 * partition + 5 * (3 + inst.n_rot))
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self, gpu_index):
+        if not self.proc:
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != gpu_index:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU arm
+def _cpu_worker(args):
+    """One process: run LGA runs of the workload through the REFERENCE library
+    (oracle/_ref) until `budget_s` elapsed; return (evals, seconds)."""
+    seeds, budget_s, kind = args
+    sys.path.insert(0, ROOT)
+    from oracle.oracle import Oracle
+
+    o = Oracle(kind)
+    inst = workload()
+    s = LgaSettings()
+    t0 = time.perf_counter()
+    evals = runs = 0
+    for sd in seeds:
+        r = o.lga_run(inst, BASELINE, SINGLE, s, int(sd))
+        evals += r["evaluations"]
+        runs += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    return evals, time.perf_counter() - t0, runs
+
+
+def cpu_measure(budget_s=12.0, procs=None):
+    import multiprocessing as mp
+
+    from oracle.oracle import available, build
+
+    kind = "reference" if available("reference") else "port"
+    if kind == "port" and not available("port"):
+        build()
+    procs = procs or os.cpu_count() or 1
+    jobs = [([10_000 + p * 1000 + k for k in range(1000)], budget_s, kind) for p in range(procs)]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    evals = sum(r[0] for r in res)
+    runs = sum(r[2] for r in res)
+    span = max(r[1] for r in res)
+    return {"value": evals / span, "unit": UNIT, "cores": procs, "kind": kind,
+            "sample": f"{runs} LGA runs of the C3 workload ({N_ATOMS} atoms/{N_ROT} torsions/{N_SITES} sites, "
+                      f"default LgaSettings, Baseline reduction) on {procs} processes x ~{budget_s:.0f} s; "
+                      f"{evals} evaluations", "wall_s": wall}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    # warmup + timed steps, each step ~3 s of CPU work on every core
+    for _ in range(args.warmup):
+        cpu_measure(1.0, procs)
+    vals = []
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_measure(3.0, procs)
+        vals.append(last["value"])
+    total = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference random_instance recipe)",
+            "config": {"workload": "C3 small-ligand docking, 100 LGA runs", "n_atoms": N_ATOMS, "n_rot": N_ROT,
+                       "n_sites": N_SITES, "lga": "default LgaSettings", "method": "baseline"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": last["kind"],
+                             "sample": last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GPU arm
+def fp64_peak_tflops(torch):
+    """Live FP64 FMA peak of this GPU (DFMA chains, no memory traffic)."""
+    src = r"""
+extern "C" __global__ void dfma_peak(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 1234.5) out[threadIdx.x] = a0;
+}
+"""
+    try:
+        from cuda.bindings import nvrtc  # noqa: F401
+    except Exception:
+        pass
+    try:
+        import cupy  # noqa: F401
+    except Exception:
+        pass
+    # compile with nvcc once into profiles-independent cache
+    cache = os.path.join(ROOT, "paper_2410_10447_b200", "build")
+    os.makedirs(cache, exist_ok=True)
+    cu = os.path.join(cache, "dfma_peak.cu")
+    cub = os.path.join(cache, "dfma_peak.cubin")
+    if not os.path.exists(cub):
+        with open(cu, "w") as f:
+            f.write(src)
+        subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-cubin",
+                        "-o", cub, cu], check=True, capture_output=True)
+    cuda = C.CDLL("libcuda.so.1")
+    mod = C.c_void_p()
+    fn = C.c_void_p()
+    torch.cuda.current_device()
+    torch.zeros(1, device="cuda")
+    assert cuda.cuModuleLoad(C.byref(mod), cub.encode()) == 0
+    assert cuda.cuModuleGetFunction(C.byref(fn), mod, b"dfma_peak") == 0
+    out = torch.zeros(1024, dtype=torch.float64, device="cuda")
+    iters = 20000
+    grid = torch.cuda.get_device_properties(0).multi_processor_count * 8
+    ptr = C.c_void_p(out.data_ptr())
+    it = C.c_int(iters)
+    params = (C.c_void_p * 2)(C.cast(C.byref(ptr), C.c_void_p), C.cast(C.byref(it), C.c_void_p))
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def launch():
+        assert cuda.cuLaunchKernel(fn, grid, 1, 1, 256, 1, 1, 0, stream, params, None) == 0
+
+    launch()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = float("inf")
+    for _ in range(5):
+        s.record()
+        launch()
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    flops = 2.0 * 8 * iters * grid * 256
+    return flops / (best * 1e-3) / 1e12
+
+
+def run_gpu_arm(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2410_10447_b200 import Device
+    from paper_2410_10447_b200._lib import load
+
+    lib = load()
+    pair = PAIR_FP32 if args.pair == "fp32" else PAIR_FP64
+    dev = Device(local, pair=pair, warps_per_block=args.wpb)
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    inst = workload()
+    settings = LgaSettings()
+    method = METHODS[args.method]
+    accum = SINGLE
+    dim = inst.dim
+    seeds_host = np.arange(N_RUNS, dtype=np.uint64) + np.uint64(1_000_000 + rank * N_RUNS)
+
+    # device-resident state: instance, seeds, the LGA batch (one CUDA graph)
+    dinst = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+    assert dinst, lib.mdr_last_error(dev.ctx)
+    batch = lib.mdr_lga_batch_create(dev.ctx, dinst, method, accum, C.byref(settings), N_RUNS)
+    assert batch, lib.mdr_last_error(dev.ctx)
+    d_seeds = torch.from_numpy(seeds_host.view(np.int64)).to(f"cuda:{local}")
+    d_total = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def step():
+        rc = lib.mdr_lga_batch_run_dev(dev.ctx, batch, C.c_void_p(d_seeds.data_ptr()))
+        assert rc == 0, lib.mdr_last_error(dev.ctx)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # evaluations per step (deterministic per seed set)
+    lib.mdr_lga_batch_total_evals_dev(dev.ctx, batch, C.c_void_p(d_total.data_ptr()))
+    torch.cuda.synchronize()
+    evals_per_step = int(d_total.item())
+
+    launches0 = dev.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk_path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp",
+                            f"clocks_rank{rank}.csv")
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(clk_path) as clk:
+        for k in range(args.steps):
+            flush.fill_(float(k))  # > L2 (126 MB): flush between timed steps
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = dev.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(step_ms)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    total_evals = evals_per_step * args.steps * world
+    value = total_evals / (t_max * 1e-3)
+
+    # ---- e2e through the reference-facing host call (host buffers)
+    maxr = settings.max_records
+    be = np.zeros(N_RUNS)
+    bg = np.zeros((N_RUNS, dim))
+    evs = np.zeros(N_RUNS, np.int64)
+    cv = np.zeros(N_RUNS, np.int32)
+    nr = np.zeros(N_RUNS, np.int32)
+    recs = (LsRecord * (N_RUNS * maxr))()
+    st = (SyncStats * N_RUNS)()
+    seeds_pinned = torch.from_numpy(seeds_host.view(np.int64)).pin_memory()
+
+    def e2e_call():
+        rc = lib.mdr_lga_run_batch(dev.ctx, C.byref(inst.c()), method, accum, C.byref(settings),
+                                   C.c_void_p(seeds_pinned.data_ptr()), N_RUNS, be.ctypes.data, bg.ctypes.data,
+                                   evs.ctypes.data, cv.ctypes.data, nr.ctypes.data, recs, st)
+        assert rc == 0, lib.mdr_last_error(dev.ctx)
+
+    e2e_call()
+    e2e_steps = max(1, min(args.steps, 5))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = int(evs.sum()) * e2e_steps * world / float(te.item())
+    h2d = inst.atoms.nbytes + inst.torsion.nbytes + inst.sites.nbytes + seeds_host.nbytes + C.sizeof(settings)
+    d2h = be.nbytes + bg.nbytes + evs.nbytes + cv.nbytes + nr.nbytes + C.sizeof(recs) + 4 * N_RUNS
+
+    # ---- dominant-kernel timing (instrumented replay, outside the timed region)
+    roof = None
+    ls_share = None
+    if hasattr(lib, "mdr_lga_batch_profile_dev"):
+        ls_ms = C.c_float()
+        all_ms = C.c_float()
+        ls_evals = C.c_int64()
+        rc = lib.mdr_lga_batch_profile_dev(dev.ctx, batch, C.c_void_p(d_seeds.data_ptr()), C.byref(ls_ms),
+                                           C.byref(all_ms), C.byref(ls_evals))
+        if rc == 0 and ls_ms.value > 0:
+            peak = fp64_peak_tflops(torch)
+            flops = flop_per_eval(inst, settings.partition) * ls_evals.value
+            achieved = flops / (ls_ms.value * 1e-3) / 1e12
+            n_ls_launches = settings.generations + 1
+            roof = {"bound": "fp64", "kernel": "lga_ls_kernel (device ADADELTA chain, warp per pose)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "peak_source": "measured live: DFMA-chain kernel on this GPU (MEASURED_PEAKS.json has no FP64 "
+                                   "figure)",
+                    "flop_per_eval": flop_per_eval(inst, settings.partition),
+                    "ls_evals_per_step": ls_evals.value, "ls_kernel_ms_per_launch": ls_ms.value / n_ls_launches,
+                    "traffic": None}
+            ls_share = ls_ms.value / all_ms.value
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            cpu = cpu_measure(args.cpu_seconds)
+        clocks = clk.summary(local)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if pair == PAIR_FP64 else "f32",
+            "data": "synthetic (reference random_instance recipe, derive_rng(12345,'synth/small'))",
+            "config": {"workload": "C3 small-ligand docking: 100 LGA runs per GPU (BASELINE.json configs[2])",
+                       "n_atoms": N_ATOMS, "n_rot": N_ROT, "n_sites": N_SITES, "runs_per_gpu": N_RUNS,
+                       "lga": "default LgaSettings (pop 36, 20 gens, LS 150 iters, partition 64)",
+                       "reduction": args.method, "pair_terms": args.pair, "parallelism": f"runs sharded x{world}",
+                       "evals_per_step_per_gpu": evals_per_step, "l2": "flushed (256 MB write) before every step"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "api": "mdr_lga_run_batch (host buffers, synchronous)"},
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "ls_kernel_share_of_step": ls_share,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "docking_sec_per_ligand": t_max * 1e-3 / args.steps,
+        }
+        if args.extra:
+            line.update(extra_measurements(args, dev, lib, torch))
+        print(json.dumps(line), flush=True)
+    lib.mdr_lga_batch_destroy(dev.ctx, batch)
+    lib.mdr_instance_free(dev.ctx, dinst)
+    if dist:
+        dist.destroy_process_group()
+
+
+def extra_measurements(args, dev, lib, torch):
+    """C2 reduction microbench (ns/call) when the bench kernels are built."""
+    out = {}
+    if hasattr(lib, "mdr_reduce_bench_dev"):
+        from paper_2410_10447_b200.microbench import reduce_microbench
+
+        out["reduce_microbench"] = reduce_microbench(dev, lib, torch)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--method", default="baseline", choices=list(METHODS))
+    ap.add_argument("--pair", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--wpb", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extra", action="store_true", default=True)
+    ap.add_argument("--no-extra", dest="extra", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

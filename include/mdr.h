@@ -104,6 +104,8 @@ void mdr_ctx_destroy(mdr_ctx* ctx);
 int mdr_ctx_set_stream(mdr_ctx* ctx, void* cuda_stream);
 void* mdr_ctx_stream(mdr_ctx* ctx);
 int mdr_ctx_set_pair_precision(mdr_ctx* ctx, int pair_precision);
+/* Warps per CTA of the warp-per-pose kernels (1..16, default 2). */
+int mdr_ctx_set_warps_per_block(mdr_ctx* ctx, int warps);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);
 /* Number of kernel launches this context has enqueued so far. */

@@ -1,0 +1,843 @@
+// capi.cpp — host implementation of the C-ABI in include/mdr.h.
+//
+// Validation mirrors the reference's exceptions (thrown before any work):
+//   BlockConfig simblock.cpp:10-19, reduce4 reduce.cpp:81-83,
+//   baseline_block_reduce reduce.cpp:138-147, reduce7 reduce.cpp:192-196,
+//   lga_run docking.cpp:395-397, adadelta_step docking.cpp:285-293.
+// SyncStats are the reference's model counters for the chosen method
+// (reduce.cpp:86-110, 149-162; docking.cpp:215-220) so the drop-in API
+// returns the values reference callers expect; real device behaviour is
+// measured by ncu (profiles/).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "dock_launch.h"
+#include "mdr.h"
+#include "mdr_shared.h"
+
+using namespace mdr;
+
+struct mdr_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int pair = MDR_PAIR_FP64;
+  int wpb = 2;  // warps per CTA of the warp-per-pose kernels
+  std::string err;
+  uint64_t launches = 0;
+};
+
+struct mdr_dev_instance {
+  LigandView view{};
+  void* block = nullptr;  // one device allocation holding every array
+  int n_atoms = 0, n_sites = 0, n_rot = 0;
+};
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(mdr_ctx* ctx, int code, const std::string& msg) {
+  t_err = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int cuda_fail(mdr_ctx* ctx, cudaError_t e, const char* where) {
+  return fail(ctx, MDR_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                            \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+  } while (0)
+
+bool legal_block(int threads, int method) {
+  const int lo = method == MDR_METHOD_TCU ? 64 : 32;
+  return threads >= lo && threads <= 1024 && threads % 32 == 0;
+}
+
+int check_partition(mdr_ctx* ctx, int partition, int method) {
+  if (method < 0 || method > 2) return fail(ctx, MDR_ERR_INVALID, "unknown reduce method");
+  if (!legal_block(partition, method))
+    return fail(ctx, MDR_ERR_BLOCK_SIZE,
+                std::string(method == MDR_METHOD_TCU ? "tcu" : "baseline") +
+                    " blocks support multiples of 32 in [" + (method == MDR_METHOD_TCU ? "64" : "32") +
+                    ", 1024], got " + std::to_string(partition));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------- model counters
+void st_zero(mdr_sync_stats* s) { std::memset(s, 0, sizeof *s); }
+void st_add(mdr_sync_stats* a, const mdr_sync_stats& b, uint64_t k = 1) {
+  a->block_syncs += k * b.block_syncs;
+  a->warp_shuffles += k * b.warp_shuffles;
+  a->atomic_adds += k * b.atomic_adds;
+  a->memory_fences += k * b.memory_fences;
+  a->mma_ops += k * b.mma_ops;
+  a->shared_mem_bytes += k * b.shared_mem_bytes;
+  a->precision_conversions += k * b.precision_conversions;
+}
+mdr_sync_stats block_stats(int threads) {  // reduce.cpp:149-162
+  mdr_sync_stats s;
+  st_zero(&s);
+  s.block_syncs = 3;
+  s.memory_fences = 2;
+  s.shared_mem_bytes = 4;
+  s.atomic_adds = (uint64_t)(threads / 32);
+  s.warp_shuffles = 160ull * (uint64_t)(threads / 32);
+  return s;
+}
+mdr_sync_stats reduce4_stats(int n, int accum) {  // reduce.cpp:84-110
+  mdr_sync_stats s;
+  st_zero(&s);
+  const uint64_t chunks = (uint64_t)((n + 63) / 64);
+  s.block_syncs = 2;
+  s.shared_mem_bytes = chunks * 64 * 4 * 2;
+  s.precision_conversions = 4ull * (uint64_t)n + (accum == MDR_ACCUM_HALF ? 4u : 256u);
+  s.mma_ops = chunks + 1;
+  return s;
+}
+// TcuSplit (new method): counts of the in-warp implementation per reduction
+// of n records with `comps` components: tf32 hi/lo conversions, one
+// m16n8k8 per 8 source lanes, a 1 KiB staging buffer, broadcast shuffles.
+mdr_sync_stats split_stats(int n, int comps) {
+  mdr_sync_stats s;
+  st_zero(&s);
+  const uint64_t groups = (uint64_t)((n + 31) / 32);
+  s.mma_ops = 4 * groups;
+  s.shared_mem_bytes = 1024;
+  s.precision_conversions = 2ull * (uint64_t)comps * (uint64_t)n;
+  s.warp_shuffles = 32ull * (uint64_t)comps;
+  return s;
+}
+mdr_sync_stats reduce7_stats(int n, int method, int accum) {
+  mdr_sync_stats s;
+  st_zero(&s);
+  if (method == MDR_METHOD_BASELINE) {
+    st_add(&s, block_stats(n), 7);
+  } else if (method == MDR_METHOD_TCU) {
+    st_add(&s, reduce4_stats(n, accum), 2);
+  } else {
+    s = split_stats(n, 7);
+  }
+  return s;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t n, cudaStream_t st) {
+    s = st;
+    if (n == 0) n = 1;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+cudaStream_t S(mdr_ctx* c) { return c->stream; }
+
+}  // namespace
+
+extern "C" {
+
+const char* mdr_version(void) { return "mdr-b200 0.1.0 (sm_100a)"; }
+
+mdr_ctx* mdr_ctx_create(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return nullptr;
+  mdr_ctx* c = new mdr_ctx;
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return nullptr;
+  }
+  c->stream = c->own;
+  return c;
+}
+
+void mdr_ctx_destroy(mdr_ctx* c) {
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  cudaStreamDestroy(c->own);
+  delete c;
+}
+
+int mdr_ctx_set_stream(mdr_ctx* c, void* s) {
+  if (!c) return MDR_ERR_INVALID;
+  c->stream = s ? static_cast<cudaStream_t>(s) : c->own;
+  return MDR_OK;
+}
+void* mdr_ctx_stream(mdr_ctx* c) { return c ? c->stream : nullptr; }
+
+int mdr_ctx_set_pair_precision(mdr_ctx* c, int p) {
+  if (!c || (p != MDR_PAIR_FP64 && p != MDR_PAIR_FP32)) return fail(c, MDR_ERR_INVALID, "bad pair precision");
+  c->pair = p;
+  return MDR_OK;
+}
+
+int mdr_ctx_set_warps_per_block(mdr_ctx* c, int wpb) {
+  if (!c || wpb < 1 || wpb > 16) return fail(c, MDR_ERR_INVALID, "warps per block must be 1..16");
+  c->wpb = wpb;
+  return MDR_OK;
+}
+
+const char* mdr_last_error(mdr_ctx* c) { return c ? c->err.c_str() : t_err.c_str(); }
+uint64_t mdr_ctx_launch_count(mdr_ctx* c) { return c ? c->launches : 0; }
+int mdr_ctx_synchronize(mdr_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- L0
+int mdr_f32_to_half_batch(mdr_ctx* ctx, const float* in, size_t n, uint16_t* out) {
+  if (!ctx || (n && (!in || !out))) return fail(ctx, MDR_ERR_INVALID, "null argument");
+  if (n == 0) return MDR_OK;
+  DevBuf<float> di;
+  DevBuf<uint16_t> dout;
+  CK(di.alloc(n, S(ctx)));
+  CK(dout.alloc(n, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, in, n * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_f32_to_half(di.p, n, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, n * 2, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_half_to_f32_batch(mdr_ctx* ctx, const uint16_t* in, size_t n, float* out) {
+  if (!ctx || (n && (!in || !out))) return fail(ctx, MDR_ERR_INVALID, "null argument");
+  if (n == 0) return MDR_OK;
+  DevBuf<uint16_t> di;
+  DevBuf<float> dout;
+  CK(di.alloc(n, S(ctx)));
+  CK(dout.alloc(n, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, in, n * 2, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_half_to_f32(di.p, n, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, n * 4, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_mma_batch(mdr_ctx* ctx, const uint16_t* a, const uint16_t* b, const float* c, int n_tiles, int accum,
+                  float* d) {
+  if (!ctx || n_tiles < 0 || (n_tiles && (!a || !b || !c || !d))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (n_tiles == 0) return MDR_OK;
+  const size_t n = (size_t)n_tiles * 256;
+  DevBuf<uint16_t> da, db;
+  DevBuf<float> dc, dd;
+  CK(da.alloc(n, S(ctx)));
+  CK(db.alloc(n, S(ctx)));
+  CK(dc.alloc(n, S(ctx)));
+  CK(dd.alloc(n, S(ctx)));
+  CK(cudaMemcpyAsync(da.p, a, n * 2, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(db.p, b, n * 2, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(dc.p, c, n * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_mma16(da.p, db.p, dc.p, n_tiles, accum == MDR_ACCUM_HALF, dd.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(d, dd.p, n * 4, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- L1
+int mdr_warp_reduce_batch(mdr_ctx* ctx, const float* lanes, int n_red, float* out, mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!lanes || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (st) {
+    st_zero(st);
+    st->warp_shuffles = 160;
+  }
+  if (n_red == 0) return MDR_OK;
+  DevBuf<float> di, dout;
+  CK(di.alloc((size_t)n_red * 32, S(ctx)));
+  CK(dout.alloc(n_red, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, lanes, (size_t)n_red * 32 * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_warp_reduce(di.p, n_red, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 4, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_block_reduce_batch(mdr_ctx* ctx, const float* values, int threads, int n_red, float* out,
+                           mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!values || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (!legal_block(threads, MDR_METHOD_BASELINE))
+    return fail(ctx, MDR_ERR_BLOCK_SIZE,
+                "baseline_block_reduce supports multiples of 32 in [32, 1024], got " + std::to_string(threads));
+  if (st) *st = block_stats(threads);
+  if (n_red == 0) return MDR_OK;
+  const size_t n = (size_t)n_red * threads;
+  DevBuf<float> di, dout;
+  CK(di.alloc(n, S(ctx)));
+  CK(dout.alloc(n_red, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, values, n * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_block_reduce(di.p, threads, n_red, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 4, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red, int method, int accum, float* out,
+                      mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!vecs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (method < 0 || method > 2) return fail(ctx, MDR_ERR_INVALID, "unknown reduce method");
+  if (n < 1) return fail(ctx, MDR_ERR_SIZE, "reduce4 requires at least one vector");
+  if (method == MDR_METHOD_BASELINE && !legal_block(n, method))
+    return fail(ctx, MDR_ERR_BLOCK_SIZE, "baseline blocks support multiples of 32 in [32, 1024], got " +
+                                             std::to_string(n));
+  if (st) {
+    if (method == MDR_METHOD_TCU) {
+      *st = reduce4_stats(n, accum);
+    } else if (method == MDR_METHOD_BASELINE) {
+      st_zero(st);
+      st_add(st, block_stats(n), 4);
+    } else {
+      *st = split_stats(n, 4);
+    }
+  }
+  if (n_red == 0) return MDR_OK;
+  const size_t cnt = (size_t)n_red * n * 4;
+  DevBuf<float> di, dout;
+  CK(di.alloc(cnt, S(ctx)));
+  CK(dout.alloc((size_t)n_red * 4, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, vecs, cnt * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_reduce4(di.p, n, n_red, method, accum == MDR_ACCUM_HALF, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 16, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int method, int accum, float* out,
+                      mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!recs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (method < 0 || method > 2) return fail(ctx, MDR_ERR_INVALID, "unknown reduce method");
+  if (method == MDR_METHOD_BASELINE && !legal_block(n, method))
+    return fail(ctx, MDR_ERR_BLOCK_SIZE, "baseline_block_reduce supports multiples of 32 in [32, 1024], got " +
+                                             std::to_string(n));
+  if (method == MDR_METHOD_TCU && n < 64)
+    return fail(ctx, MDR_ERR_BLOCK_SIZE,
+                "tcu reduce7 needs at least 64 records (a full 16x16 tile), got " + std::to_string(n));
+  if (method == MDR_METHOD_TCU_SPLIT && n < 1) return fail(ctx, MDR_ERR_SIZE, "reduce7 needs records");
+  if (st) *st = reduce7_stats(n, method, accum);
+  if (n_red == 0) return MDR_OK;
+  const size_t cnt = (size_t)n_red * n * 7;
+  DevBuf<float> di, dout;
+  CK(di.alloc(cnt, S(ctx)));
+  CK(dout.alloc((size_t)n_red * 7, S(ctx)));
+  CK(cudaMemcpyAsync(di.p, recs, cnt * 4, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_reduce7(di.p, n, n_red, method, accum == MDR_ACCUM_HALF, dout.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 28, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- ligand
+static void torsion_axis_host(int k, double* out) {  // docking.cpp:181-189 (glibc, like the reference)
+  constexpr double kGolden = 2.399963229728653;
+  const double az = kGolden * k + 0.3;
+  const double zc = 0.5 + 0.35 * std::sin(0.9 * k + 0.4);
+  const double v[3] = {0.8 * std::cos(az), 0.8 * std::sin(az), zc};
+  const double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+  out[0] = v[0] / n;
+  out[1] = v[1] / n;
+  out[2] = v[2] / n;
+}
+
+static int check_instance(mdr_ctx* ctx, const mdr_instance* in) {
+  if (!in || !in->atom_xyzw || !in->atom_torsion || !in->site_xyzdd)
+    return fail(ctx, MDR_ERR_INVALID, "null instance");
+  if (in->n_atoms < 1 || in->n_sites < 1) return fail(ctx, MDR_ERR_SIZE, "instance needs atoms and sites");
+  if (in->n_rot < 0 || in->n_rot > kMaxRot)
+    return fail(ctx, MDR_ERR_SIZE, "n_rot must be in [0, " + std::to_string(kMaxRot) + "] on the device path");
+  if (in->n_sites > kMaxSites || in->n_atoms > kMaxAtoms)
+    return fail(ctx, MDR_ERR_SIZE, "instance exceeds the device limits (sites <= 2048, atoms <= 4096)");
+  for (int i = 0; i < in->n_atoms; ++i)
+    if (in->atom_torsion[i] >= in->n_rot || in->atom_torsion[i] < -1)
+      return fail(ctx, MDR_ERR_SIZE, "atom references a torsion outside [0, n_rot)");
+  return MDR_OK;
+}
+
+mdr_dev_instance* mdr_instance_upload(mdr_ctx* ctx, const mdr_instance* in) {
+  if (!ctx || check_instance(ctx, in) != MDR_OK) return nullptr;
+  const int na = in->n_atoms, ns = in->n_sites, nr = in->n_rot;
+  std::vector<SiteD> sites(ns);
+  std::vector<float4> sf(ns);
+  std::vector<float2> sf2(ns);
+  double lo[3] = {std::numeric_limits<double>::max(), std::numeric_limits<double>::max(),
+                  std::numeric_limits<double>::max()};
+  double hi[3] = {std::numeric_limits<double>::lowest(), std::numeric_limits<double>::lowest(),
+                  std::numeric_limits<double>::lowest()};
+  double max_d0 = 0.0;
+  for (int j = 0; j < ns; ++j) {
+    const double* s = in->site_xyzdd + 5 * j;
+    const double d0 = s[4];
+    SiteD& o = sites[j];
+    o.x = s[0];
+    o.y = s[1];
+    o.z = s[2];
+    o.depth = s[3];
+    o.c2 = 0.5625 * d0 * d0;  // docking.cpp:114
+    o.num = d0 * d0 + o.c2;   // docking.cpp:116
+    sf[j] = {(float)s[0], (float)s[1], (float)s[2], (float)s[3]};
+    sf2[j] = {(float)o.c2, (float)o.num};
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], s[a]);
+      hi[a] = std::max(hi[a], s[a]);
+    }
+    max_d0 = std::max(max_d0, d0);
+  }
+  std::vector<double> taxes(3 * (size_t)std::max(nr, 1));
+  for (int k = 0; k < nr; ++k) torsion_axis_host(k, &taxes[3 * k]);
+  // one allocation: sites | atoms | taxes | tors | sites_f | sites_f2
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t o_sites = 0, b_sites = al(sizeof(SiteD) * ns);
+  const size_t o_atoms = o_sites + b_sites, b_atoms = al(sizeof(double4) * na);
+  const size_t o_tax = o_atoms + b_atoms, b_tax = al(sizeof(double) * taxes.size());
+  const size_t o_tors = o_tax + b_tax, b_tors = al(sizeof(int) * na);
+  const size_t o_sf = o_tors + b_tors, b_sf = al(sizeof(float4) * ns);
+  const size_t o_sf2 = o_sf + b_sf, b_sf2 = al(sizeof(float2) * ns);
+  const size_t total = o_sf2 + b_sf2;
+  mdr_dev_instance* di = new mdr_dev_instance;
+  if (cudaMalloc(&di->block, total) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "cudaMalloc failed for instance");
+    delete di;
+    return nullptr;
+  }
+  char* b = static_cast<char*>(di->block);
+  cudaStream_t s = ctx->stream;
+  cudaMemcpyAsync(b + o_sites, sites.data(), sizeof(SiteD) * ns, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_atoms, in->atom_xyzw, sizeof(double) * 4 * na, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_tax, taxes.data(), sizeof(double) * taxes.size(), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_tors, in->atom_torsion, sizeof(int) * na, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_sf, sf.data(), sizeof(float4) * ns, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(b + o_sf2, sf2.data(), sizeof(float2) * ns, cudaMemcpyHostToDevice, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "instance upload failed");
+    cudaFree(di->block);
+    delete di;
+    return nullptr;
+  }
+  LigandView& L = di->view;
+  L.n_atoms = na;
+  L.n_sites = ns;
+  L.n_rot = nr;
+  L.sites = reinterpret_cast<const SiteD*>(b + o_sites);
+  L.atoms = reinterpret_cast<const double4*>(b + o_atoms);
+  L.taxes = reinterpret_cast<const double*>(b + o_tax);
+  L.tors = reinterpret_cast<const int*>(b + o_tors);
+  L.sites_f = reinterpret_cast<const float4*>(b + o_sf);
+  L.sites_f2 = reinterpret_cast<const float2*>(b + o_sf2);
+  const double margin = max_d0 + 1.0;  // random_genotype docking.cpp:374
+  for (int a = 0; a < 3; ++a) {
+    L.box_lo[a] = lo[a] - margin;
+    L.box_hi[a] = hi[a] + margin;
+  }
+  di->n_atoms = na;
+  di->n_sites = ns;
+  di->n_rot = nr;
+  return di;
+}
+
+void mdr_instance_free(mdr_ctx* ctx, mdr_dev_instance* di) {
+  if (!di) return;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  cudaFree(di->block);
+  delete di;
+}
+
+struct InstanceGuard {
+  mdr_ctx* ctx;
+  mdr_dev_instance* di;
+  ~InstanceGuard() { mdr_instance_free(ctx, di); }
+};
+
+// ---------------------------------------------------------------- L2
+static mdr_sync_stats score_stats(int method, int accum, int partition) {
+  return reduce7_stats(partition, method, accum);
+}
+
+int mdr_score_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* g, int n, int method, int accum,
+                  int partition, float* e, float* grad, float* tq) {
+  if (!ctx || !di) return fail(ctx, MDR_ERR_INVALID, "null argument");
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (n <= 0) return MDR_OK;
+  CK(launch_score(di->view, g, n, method, ctx->pair, partition, accum == MDR_ACCUM_HALF, e, grad, tq, ctx->stream,
+                  ctx->wpb));
+  ctx->launches++;
+  return MDR_OK;
+}
+
+int mdr_score_batch(mdr_ctx* ctx, const mdr_instance* inst, const double* genos, int n, int method, int accum,
+                    int partition, float* energy, float* gradient, float* torque, mdr_sync_stats* st) {
+  if (!ctx || n < 0 || (n && (!genos || !energy || !gradient || !torque)))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (st) *st = score_stats(method, accum, partition);
+  if (n == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> dg;
+  DevBuf<float> de, dgr, dt;
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dgr.alloc((size_t)n * dim, S(ctx)));
+  CK(dt.alloc((size_t)n * 3, S(ctx)));
+  CK(cudaMemcpyAsync(dg.p, genos, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  if (int rc = mdr_score_dev(ctx, ig.di, dg.p, n, method, accum, partition, de.p, dgr.p, dt.p)) return rc;
+  CK(cudaMemcpyAsync(energy, de.p, sizeof(float) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(gradient, dgr.p, sizeof(float) * n * dim, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(torque, dt.p, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_score_reference_batch(mdr_ctx* ctx, const mdr_instance* inst, const double* genos, int n, double* energy,
+                              double* gradient, double* torque) {
+  if (!ctx || n < 0 || (n && (!genos || !energy || !gradient || !torque)))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  if (n == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> dg, de, dgr, dt;
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dgr.alloc((size_t)n * dim, S(ctx)));
+  CK(dt.alloc((size_t)n * 3, S(ctx)));
+  CK(cudaMemcpyAsync(dg.p, genos, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_score_reference(ig.di->view, dg.p, n, de.p, dgr.p, dt.p, S(ctx), ctx->wpb));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(energy, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(gradient, dgr.p, sizeof(double) * n * dim, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(torque, dt.p, sizeof(double) * n * 3, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- L3
+int mdr_adadelta_step_batch(mdr_ctx* ctx, int dim, int n, double rho, double eps, double* sq_g, double* sq_u,
+                            double* geno, const double* grad) {
+  if (!ctx || dim < 6 || dim > kMaxDim || n < 0 || (n && (!sq_g || !sq_u || !geno || !grad)))
+    return fail(ctx, MDR_ERR_SIZE, "adadelta_step: state/gradient dimensions do not match genotype");
+  if (n == 0) return MDR_OK;
+  const size_t cnt = (size_t)n * dim;
+  // NumericDomainError is raised before any state changes (docking.cpp:289-293)
+  for (size_t i = 0; i < cnt; ++i)
+    if (!std::isfinite(grad[i])) return fail(ctx, MDR_ERR_NUMERIC_DOMAIN, "adadelta_step: non-finite gradient component");
+  DevBuf<double> a, b, g, gr;
+  DevBuf<int> stt;
+  CK(a.alloc(cnt, S(ctx)));
+  CK(b.alloc(cnt, S(ctx)));
+  CK(g.alloc(cnt, S(ctx)));
+  CK(gr.alloc(cnt, S(ctx)));
+  CK(stt.alloc(n, S(ctx)));
+  CK(cudaMemsetAsync(stt.p, 0, sizeof(int) * n, S(ctx)));
+  CK(cudaMemcpyAsync(a.p, sq_g, cnt * 8, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(b.p, sq_u, cnt * 8, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(g.p, geno, cnt * 8, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(gr.p, grad, cnt * 8, cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_adadelta(dim, n, rho, eps, a.p, b.p, g.p, gr.p, stt.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(sq_g, a.p, cnt * 8, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(sq_u, b.p, cnt * 8, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(geno, g.p, cnt * 8, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* starts, int n, int max_iters,
+                         double tol, int method, int accum, int partition, double* og, double* oe, int32_t* oit,
+                         int32_t* ocv, int32_t* status) {
+  if (!ctx || !di || max_iters < 0) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (n <= 0) return MDR_OK;
+  CK(launch_local_search(di->view, starts, n, max_iters, tol, method, ctx->pair, partition, accum == MDR_ACCUM_HALF,
+                         og, oe, oit, ocv, status, ctx->stream, ctx->wpb));
+  ctx->launches++;
+  return MDR_OK;
+}
+
+int mdr_local_search_batch(mdr_ctx* ctx, const mdr_instance* inst, const double* starts, int n, int max_iters,
+                           double tol, int method, int accum, int partition, double* out_g, double* out_e,
+                           int32_t* out_it, int32_t* out_cv, mdr_sync_stats* st) {
+  if (!ctx || n < 0 || max_iters < 0 || (n && (!starts || !out_g || !out_e || !out_it || !out_cv)))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (n == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> ds, dg, de;
+  DevBuf<int> dit, dcv, dst;
+  CK(ds.alloc((size_t)n * dim, S(ctx)));
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dit.alloc(n, S(ctx)));
+  CK(dcv.alloc(n, S(ctx)));
+  CK(dst.alloc(n, S(ctx)));
+  CK(cudaMemsetAsync(dst.p, 0, sizeof(int) * n, S(ctx)));
+  CK(cudaMemcpyAsync(ds.p, starts, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  if (int rc = mdr_local_search_dev(ctx, ig.di, ds.p, n, max_iters, tol, method, accum, partition, dg.p, de.p, dit.p,
+                                    dcv.p, dst.p))
+    return rc;
+  std::vector<int> status(n);
+  CK(cudaMemcpyAsync(out_g, dg.p, sizeof(double) * n * dim, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_e, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_it, dit.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_cv, dcv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(status.data(), dst.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  for (int i = 0; i < n; ++i)
+    if (status[i] != MDR_OK) return fail(ctx, status[i], "adadelta_step: non-finite gradient component");
+  if (st) {
+    const mdr_sync_stats one = score_stats(method, accum, partition);
+    for (int i = 0; i < n; ++i) {
+      st_zero(&st[i]);
+      st_add(&st[i], one, (uint64_t)out_it[i] + 1);
+    }
+  }
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- LGA
+void mdr_lga_defaults(mdr_lga_settings* s) {  // docking.hpp:106-115
+  s->population_size = 36;
+  s->generations = 20;
+  s->max_evaluations = 100000;
+  s->ls_fraction = 0.25;
+  s->ls_max_iters = 150;
+  s->partition = 64;
+  s->ls_convergence_tol = 1e-4;
+  s->mutation_sigma = 0.3;
+}
+
+static int ls_count_of(const mdr_lga_settings* s) {  // docking.cpp:424-426
+  const int off = s->population_size - 1;
+  return std::clamp(static_cast<int>(std::ceil(s->ls_fraction * off)), 0, off);
+}
+
+int mdr_lga_max_records(const mdr_lga_settings* s) { return s->generations * ls_count_of(s) + 1; }
+
+struct mdr_lga_batch {
+  LgaDev D{};
+  LigandView L{};
+  int method = 0, pair = 0, accum = 0;
+  void* block = nullptr;
+  uint64_t* seeds = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t captured_on = nullptr;
+  int launches = 0;
+  mdr_lga_settings settings{};
+};
+
+static uint64_t mix64_host(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t label_hash(const char* label) {  // mix64(fnv1a64(label)), rng.cpp:11-32
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (const unsigned char* p = reinterpret_cast<const unsigned char*>(label); *p; ++p) h = (h ^ *p) * 0x100000001b3ull;
+  return mix64_host(h);
+}
+
+static int check_lga(mdr_ctx* ctx, int method, const mdr_lga_settings* s) {
+  if (!s) return fail(ctx, MDR_ERR_INVALID, "null settings");
+  if (s->population_size < 2) return fail(ctx, MDR_ERR_SIZE, "lga_run needs a population of at least 2");
+  if (s->generations < 0 || s->ls_max_iters < 0) return fail(ctx, MDR_ERR_INVALID, "negative generations/iters");
+  return check_partition(ctx, s->partition, method);
+}
+
+mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, int method, int accum,
+                                    const mdr_lga_settings* s, int R) {
+  if (!ctx || !di || R <= 0) {
+    fail(ctx, MDR_ERR_INVALID, "bad argument");
+    return nullptr;
+  }
+  if (check_lga(ctx, method, s)) return nullptr;
+  mdr_lga_batch* b = new mdr_lga_batch;
+  b->L = di->view;
+  b->method = method;
+  b->pair = ctx->pair;
+  b->accum = accum;
+  b->settings = *s;
+  LgaDev& D = b->D;
+  D.R = R;
+  D.P = s->population_size;
+  D.dim = 6 + di->n_rot;
+  D.off = D.P - 1;
+  D.L = ls_count_of(s);
+  D.gens = s->generations;
+  D.ls_iters = s->ls_max_iters;
+  D.maxrec = mdr_lga_max_records(s);
+  D.partition = s->partition;
+  D.half_mode = accum == MDR_ACCUM_HALF;
+  D.max_evals = s->max_evaluations;
+  D.tol = s->ls_convergence_tol;
+  D.sigma = s->mutation_sigma;
+  D.label_hash = label_hash("lga");
+  const size_t dim = D.dim, P = D.P, L = std::max(D.L, 1), Rr = R;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  size_t off = 0;
+  std::vector<std::pair<void**, size_t>> parts;
+  double *pop0, *pop1, *pe0, *pe1;
+  parts.push_back({(void**)&pop0, sizeof(double) * Rr * P * dim});
+  parts.push_back({(void**)&pop1, sizeof(double) * Rr * P * dim});
+  parts.push_back({(void**)&pe0, sizeof(double) * Rr * P});
+  parts.push_back({(void**)&pe1, sizeof(double) * Rr * P});
+  parts.push_back({(void**)&D.cur, sizeof(int) * Rr});
+  parts.push_back({(void**)&D.lsg, sizeof(double) * Rr * L * dim});
+  parts.push_back({(void**)&D.lse, sizeof(double) * Rr * L});
+  parts.push_back({(void**)&D.lsit, sizeof(int) * Rr * L});
+  parts.push_back({(void**)&D.lscv, sizeof(int) * Rr * L});
+  parts.push_back({(void**)&D.lstarget, sizeof(int) * Rr * L});
+  parts.push_back({(void**)&D.best_e, sizeof(double) * Rr});
+  parts.push_back({(void**)&D.best_g, sizeof(double) * Rr * dim});
+  parts.push_back({(void**)&D.evals, sizeof(long long) * Rr});
+  parts.push_back({(void**)&D.active, sizeof(int) * Rr});
+  parts.push_back({(void**)&D.nrec, sizeof(int) * Rr});
+  parts.push_back({(void**)&D.recs, sizeof(mdr_ls_record) * Rr * D.maxrec});
+  parts.push_back({(void**)&D.conv, sizeof(int) * Rr});
+  parts.push_back({(void**)&D.status, sizeof(int) * Rr});
+  parts.push_back({(void**)&b->seeds, sizeof(uint64_t) * Rr});
+  for (auto& p : parts) off += al(p.second);
+  if (cudaMalloc(&b->block, off) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "cudaMalloc failed for LGA batch");
+    delete b;
+    return nullptr;
+  }
+  off = 0;
+  for (auto& p : parts) {
+    *p.first = static_cast<char*>(b->block) + off;
+    off += al(p.second);
+  }
+  D.pop[0] = pop0;
+  D.pop[1] = pop1;
+  D.pope[0] = pe0;
+  D.pope[1] = pe1;
+  D.seeds = b->seeds;
+  // capture the whole docking (init, gens x {offspring, LS, finalize}, polish)
+  // into one CUDA graph, replayed per call
+  cudaStream_t cs;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "stream create failed");
+    cudaFree(b->block);
+    delete b;
+    return nullptr;
+  }
+  cudaError_t e = prepare_lga(b->L, method, b->pair, ctx->wpb);
+  if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) e = launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, &b->launches);
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&b->exec, g, 0);
+  cudaStreamDestroy(cs);
+  b->graph = g;
+  if (e != cudaSuccess) {
+    cuda_fail(ctx, e, "LGA graph capture");
+    if (g) cudaGraphDestroy(g);
+    cudaFree(b->block);
+    delete b;
+    return nullptr;
+  }
+  return b;
+}
+
+void mdr_lga_batch_destroy(mdr_ctx* ctx, mdr_lga_batch* b) {
+  if (!b) return;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  if (b->exec) cudaGraphExecDestroy(b->exec);
+  if (b->graph) cudaGraphDestroy(b->graph);
+  cudaFree(b->block);
+  delete b;
+}
+
+int mdr_lga_batch_run_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds) {
+  if (!ctx || !b || !d_seeds) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  CK(cudaMemcpyAsync(b->seeds, d_seeds, sizeof(uint64_t) * b->D.R, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaGraphLaunch(b->exec, ctx->stream));
+  ctx->launches += (uint64_t)b->launches;
+  return MDR_OK;
+}
+
+int mdr_lga_batch_total_evals_dev(mdr_ctx* ctx, mdr_lga_batch* b, int64_t* d_total) {
+  if (!ctx || !b || !d_total) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  CK(launch_lga_total(b->D, reinterpret_cast<long long*>(d_total), ctx->stream));
+  ctx->launches++;
+  return MDR_OK;
+}
+
+int mdr_lga_batch_download(mdr_ctx* ctx, mdr_lga_batch* b, double* best_e, double* best_g, int64_t* evals,
+                           int32_t* conv, int32_t* n_records, mdr_ls_record* records, mdr_sync_stats* total) {
+  if (!ctx || !b) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  const LgaDev& D = b->D;
+  std::vector<int> status(D.R);
+  if (best_e) CK(cudaMemcpyAsync(best_e, D.best_e, sizeof(double) * D.R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (best_g)
+    CK(cudaMemcpyAsync(best_g, D.best_g, sizeof(double) * D.R * D.dim, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<long long> ev(D.R);
+  CK(cudaMemcpyAsync(ev.data(), D.evals, sizeof(long long) * D.R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (conv) CK(cudaMemcpyAsync(conv, D.conv, sizeof(int) * D.R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (n_records) CK(cudaMemcpyAsync(n_records, D.nrec, sizeof(int) * D.R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (records)
+    CK(cudaMemcpyAsync(records, D.recs, sizeof(mdr_ls_record) * D.R * D.maxrec, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  CK(cudaMemcpyAsync(status.data(), D.status, sizeof(int) * D.R, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int r = 0; r < D.R; ++r) {
+    if (evals) evals[r] = ev[r];
+    if (total) {
+      st_zero(&total[r]);
+      st_add(&total[r], score_stats(b->method, b->accum, D.partition), (uint64_t)ev[r]);
+    }
+  }
+  for (int r = 0; r < D.R; ++r)
+    if (status[r] != MDR_OK) return fail(ctx, status[r], "adadelta_step: non-finite gradient component");
+  return MDR_OK;
+}
+
+int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int accum, const mdr_lga_settings* s,
+                      const uint64_t* seeds, int n_runs, double* best_e, double* best_g, int64_t* evals,
+                      int32_t* conv, int32_t* n_records, mdr_ls_record* records, mdr_sync_stats* total) {
+  if (!ctx || n_runs < 0 || (n_runs && !seeds)) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  if (int rc = check_lga(ctx, method, s)) return rc;
+  if (n_runs == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  mdr_lga_batch* b = mdr_lga_batch_create(ctx, ig.di, method, accum, s, n_runs);
+  if (!b) return MDR_ERR_CUDA;
+  DevBuf<uint64_t> ds;
+  int rc = MDR_OK;
+  if (ds.alloc(n_runs, S(ctx)) != cudaSuccess ||
+      cudaMemcpyAsync(ds.p, seeds, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, S(ctx)) != cudaSuccess)
+    rc = fail(ctx, MDR_ERR_CUDA, "seed upload failed");
+  if (rc == MDR_OK) rc = mdr_lga_batch_run_dev(ctx, b, ds.p);
+  if (rc == MDR_OK) rc = mdr_lga_batch_download(ctx, b, best_e, best_g, evals, conv, n_records, records, total);
+  mdr_lga_batch_destroy(ctx, b);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,603 @@
+// dock.cu — scoring, ADADELTA local search and LGA kernels (warp per pose).
+//
+// K3 score_kernel        : score() docking.cpp:191-233, one warp per genotype
+// K3r scoreref_kernel    : score_reference() docking.cpp:235-270
+// K4 ls_kernel           : local_search() docking.cpp:310-351, the whole
+//                          <= max_iters+1 evaluation chain stays on the device
+// K5 lga_* kernels       : lga_run() docking.cpp:392-517 split into per-phase
+//                          kernels over all runs (init, offspring, LS,
+//                          finalize, polish), captured once into a CUDA graph.
+// Compiled with --fmad=false (see mdr_device.cuh).
+#include <cuda_runtime.h>
+
+#include "dock_launch.h"
+#include "mdr_device.cuh"
+
+namespace mdr {
+
+// Per-warp shared-memory region: scratch | genotype | best genotype.
+constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8;
+
+struct WarpCtx {
+  WarpScratch ws;
+  double* g;
+  double* best;
+};
+
+__device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp) {
+  unsigned char* p = base + (size_t)warp * kWarpRegion;
+  WarpCtx w;
+  w.ws.tile = reinterpret_cast<__half*>(p);
+  w.ws.rec = reinterpret_cast<float*>(p + 2 * 256 * 2);
+  w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
+  w.best = w.g + kMaxDim;
+  return w;
+}
+
+// --------------------------------------------------------------- K3 score
+template <int METHOD, int PAIR>
+__global__ void score_kernel(LigandView L, const double* __restrict__ genos, int n, int partition, int half_mode,
+                             float* __restrict__ energy, float* __restrict__ grad, float* __restrict__ torque) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= n) return;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const int dim = 6 + L.n_rot;
+  const double* g = genos + (size_t)item * dim;
+  Frame f;
+  const ScoreOut o = score_sums<METHOD, PAIR>(S, g, partition, half_mode != 0, w.ws, f);
+  for (int d = lane; d < dim; d += 32) grad[(size_t)item * dim + d] = project_dim(S, f, o, d);
+  if (lane == 0) {
+    energy[item] = o.sums[0];
+    torque[3 * (size_t)item] = o.sums[4];
+    torque[3 * (size_t)item + 1] = o.sums[5];
+    torque[3 * (size_t)item + 2] = o.sums[6];
+  }
+}
+
+// ------------------------------------------------- K3r score_reference
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  return v;
+}
+
+__global__ void scoreref_kernel(LigandView L, const double* __restrict__ genos, int n, double* __restrict__ energy,
+                                double* __restrict__ grad, double* __restrict__ torque) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= n) return;
+  const int dim = 6 + L.n_rot;
+  const double* g = genos + (size_t)item * dim;
+  const Frame f = build_frame(g[3], g[4], g[5]);
+  const d3 tr = {g[0], g[1], g[2]};
+  double e = 0.0;
+  d3 gs = {0, 0, 0}, ts = {0, 0, 0};
+  for (int i = lane; i < S.n_atoms; i += 32) {
+    const Partial p = atom_partial_fp64(S, g, f.R, tr, i);
+    e += p.e;
+    gs = gs + p.g;
+    ts = ts + p.t;
+  }
+  e = warp_sum_d(e);
+  gs = {warp_sum_d(gs.x), warp_sum_d(gs.y), warp_sum_d(gs.z)};
+  ts = {warp_sum_d(ts.x), warp_sum_d(ts.y), warp_sum_d(ts.z)};
+  // exact per-group torsion torque (docking.cpp:244-268): reduce group k
+  for (int k = 0; k < S.n_rot; ++k) {
+    d3 tk = {0, 0, 0};
+    for (int i = lane; i < S.n_atoms; i += 32)
+      if (S.tors[i] == k) tk = tk + atom_partial_fp64(S, g, f.R, tr, i).t;
+    tk = {warp_sum_d(tk.x), warp_sum_d(tk.y), warp_sum_d(tk.z)};
+    if (lane == 0) {
+      const d3 ax = mv(f.R, d3{S.taxes[3 * k], S.taxes[3 * k + 1], S.taxes[3 * k + 2]});
+      grad[(size_t)item * dim + 6 + k] = dot(ax, tk);
+    }
+  }
+  if (lane == 0) {
+    energy[item] = e;
+    double* go = grad + (size_t)item * dim;
+    go[0] = gs.x;
+    go[1] = gs.y;
+    go[2] = gs.z;
+    go[3] = dot(d3{0.0, 0.0, 1.0}, ts);
+    go[4] = dot(f.ax_theta, ts);
+    go[5] = dot(f.ax_alpha, ts);
+    torque[3 * (size_t)item] = ts.x;
+    torque[3 * (size_t)item + 1] = ts.y;
+    torque[3 * (size_t)item + 2] = ts.z;
+  }
+}
+
+// ---------------------------------------------------------- ADADELTA
+// adadelta_step docking.cpp:297-305 for the lane-owned dimension d.
+__device__ __forceinline__ void adadelta_dim(double& sq_g, double& sq_u, double& x, double gd, int d, double rho,
+                                             double eps) {
+  const double old_u = sq_u;
+  sq_g = rho * sq_g + (1.0 - rho) * gd * gd;
+  const double delta = -sqrt(old_u + eps) / sqrt(sq_g + eps) * gd;
+  sq_u = rho * old_u + (1.0 - rho) * delta * delta;
+  x = x + delta;
+  if (d >= 3) x = wrap_angle(x);  // normalize_angles docking.cpp:172-179
+}
+
+__global__ void adadelta_kernel(int dim, int n, double rho, double eps, double* sq_g, double* sq_u, double* geno,
+                                const double* grad, int* status) {
+  const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (item >= n) return;
+  const size_t o = (size_t)item * dim;
+  bool bad = false;
+  for (int d = lane; d < dim; d += 32) bad |= !isfinite(grad[o + d]);
+  if (__any_sync(kFull, bad)) {
+    if (lane == 0) status[item] = MDR_ERR_NUMERIC_DOMAIN;
+    return;
+  }
+  for (int d = lane; d < dim; d += 32) {
+    double a = sq_g[o + d], b = sq_u[o + d], x = geno[o + d];
+    adadelta_dim(a, b, x, grad[o + d], d, rho, eps);
+    sq_g[o + d] = a;
+    sq_u[o + d] = b;
+    geno[o + d] = x;
+  }
+}
+
+// ------------------------------------------------------- K4 local search
+struct LsResult {
+  double energy;
+  int iterations, converged, status;
+};
+
+// local_search docking.cpp:310-351 run by the calling warp.  start: global
+// or shared genotype.  On return w.best holds the best genotype.
+template <int METHOD, int PAIR>
+__device__ LsResult local_search_warp(const SmemLigand& S, const double* start, int max_iters, double tol,
+                                      int partition, bool half_mode, const WarpCtx& w) {
+  const int lane = threadIdx.x & 31;
+  const int dim = 6 + S.n_rot;
+  const double rho = 0.95, eps = 1e-6;  // AdadeltaState::fresh docking.hpp:67-74
+  for (int d = lane; d < dim; d += 32) {
+    const double x = d >= 3 ? wrap_angle(start[d]) : start[d];
+    w.g[d] = x;
+    w.best[d] = x;
+  }
+  __syncwarp();
+  double sg0 = 0.0, su0 = 0.0, sg1 = 0.0, su1 = 0.0;
+  Frame f;
+  ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, partition, half_mode, w.ws, f);
+  float gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
+  float gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+  LsResult r;
+  r.energy = (double)o.sums[0];
+  r.iterations = 0;
+  r.converged = 0;
+  r.status = MDR_OK;
+  double hist = r.energy;  // ring slot `lane` holds best_history[iter] for iter % 16 == lane
+  for (int iter = 1; iter <= max_iters; ++iter) {
+    const bool bad = (lane < dim && !isfinite(gr0)) || (lane + 32 < dim && !isfinite(gr1));
+    if (__any_sync(kFull, bad)) {
+      r.status = MDR_ERR_NUMERIC_DOMAIN;
+      break;
+    }
+    __syncwarp();
+    if (lane < dim) {
+      double x = w.g[lane];
+      adadelta_dim(sg0, su0, x, (double)gr0, lane, rho, eps);
+      w.g[lane] = x;
+    }
+    if (lane + 32 < dim) {
+      double x = w.g[lane + 32];
+      adadelta_dim(sg1, su1, x, (double)gr1, lane + 32, rho, eps);
+      w.g[lane + 32] = x;
+    }
+    __syncwarp();
+    o = score_sums<METHOD, PAIR>(S, w.g, partition, half_mode, w.ws, f);
+    gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
+    gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+    if ((double)o.sums[0] < r.energy) {
+      r.energy = (double)o.sums[0];
+      for (int d = lane; d < dim; d += 32) w.best[d] = w.g[d];
+    }
+    const int slot = iter & (kWindow - 1);
+    const double old = __shfl_sync(kFull, hist, slot);  // best_history[iter - 16]
+    if (lane == slot) hist = r.energy;
+    r.iterations = iter;
+    if (iter >= kWindow && old - r.energy < tol) {
+      r.converged = 1;
+      break;
+    }
+  }
+  __syncwarp();
+  return r;
+}
+
+template <int METHOD, int PAIR>
+__global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n, int max_iters, double tol,
+                          int partition, int half_mode, double* __restrict__ out_g, double* __restrict__ out_e,
+                          int* __restrict__ out_it, int* __restrict__ out_cv, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= n) return;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const int dim = 6 + L.n_rot;
+  const LsResult r = local_search_warp<METHOD, PAIR>(S, starts + (size_t)item * dim, max_iters, tol, partition,
+                                                     half_mode != 0, w);
+  for (int d = lane; d < dim; d += 32) out_g[(size_t)item * dim + d] = w.best[d];
+  if (lane == 0) {
+    out_e[item] = r.energy;
+    out_it[item] = r.iterations;
+    out_cv[item] = r.converged;
+    if (r.status != MDR_OK) status[item] = r.status;
+  }
+}
+
+// ------------------------------------------------------------- K5 LGA
+__device__ __forceinline__ uint64_t run_key(const LgaDev& D, int run) {
+  return mix64(D.seeds[run] ^ D.label_hash);  // RngStream ctor rng.cpp:31-32
+}
+
+// lga init: random_genotype docking.cpp:360-388 + score, warp per individual.
+template <int METHOD, int PAIR>
+__global__ void lga_init_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= D.R * D.P) return;
+  const int run = item / D.P, p = item % D.P;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const uint64_t key = run_key(D, run);
+  for (int d = lane; d < D.dim; d += 32) {
+    const uint64_t n = (uint64_t)p * D.dim + d + 1;
+    double x;
+    if (d < 3)
+      x = L.box_lo[d] + (L.box_hi[d] - L.box_lo[d]) * draw_unit(key, n);
+    else
+      x = -kPi + (kPi - -kPi) * draw_unit(key, n);
+    w.g[d] = x;
+    D.pop[0][((size_t)run * D.P + p) * D.dim + d] = x;
+  }
+  __syncwarp();
+  Frame f;
+  const ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
+  if (lane == 0) D.pope[0][(size_t)run * D.P + p] = (double)o.sums[0];
+}
+
+__device__ __forceinline__ void track_best(const LgaDev& D, int run, const double* g, double e) {
+  if (e < D.best_e[run]) {  // strict: first occurrence wins (docking.cpp:408-413)
+    D.best_e[run] = e;
+    for (int d = 0; d < D.dim; ++d) D.best_g[(size_t)run * D.dim + d] = g[d];
+  }
+}
+
+__device__ __forceinline__ bool budget_ok(const LgaDev& D, long long evals) {
+  // docking.cpp:430-435
+  return evals + D.off + (long long)D.L * (D.ls_iters + 1) <= D.max_evals;
+}
+
+__global__ void lga_init_finalize(LgaDev D) {
+  const int run = blockIdx.x * blockDim.x + threadIdx.x;
+  if (run >= D.R) return;
+  D.best_e[run] = 1.7976931348623157e308;  // numeric_limits<double>::max()
+  for (int d = 0; d < D.dim; ++d) D.best_g[(size_t)run * D.dim + d] = 0.0;
+  for (int p = 0; p < D.P; ++p)
+    track_best(D, run, D.pop[0] + ((size_t)run * D.P + p) * D.dim, D.pope[0][(size_t)run * D.P + p]);
+  D.evals[run] = D.P;
+  D.cur[run] = 0;
+  D.nrec[run] = 0;
+  D.conv[run] = 0;
+  D.status[run] = MDR_OK;
+  D.active[run] = D.gens > 0 && budget_ok(D, D.P);
+}
+
+// One offspring per warp: elitism, two binary tournaments, per-dimension
+// arithmetic crossover, Gaussian mutation, angle normalisation, score
+// (docking.cpp:437-472).  Draw offsets: every generation consumes
+// off * (4 + 3*dim) draws after the P*dim initial ones.
+template <int METHOD, int PAIR>
+__global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= D.R * D.off) return;
+  const int run = item / D.off, i = item % D.off;
+  if (!D.active[run]) return;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const int c = D.cur[run];
+  const double* pop = D.pop[c] + (size_t)run * D.P * D.dim;
+  const double* pe = D.pope[c] + (size_t)run * D.P;
+  double* nxt = D.pop[c ^ 1] + (size_t)run * D.P * D.dim;
+  double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
+  if (i == 0) {  // elitism of one: first index of the strict minimum
+    double be = pe[0];
+    int bi = 0;
+    for (int p = 1; p < D.P; ++p)
+      if (pe[p] < be) {
+        be = pe[p];
+        bi = p;
+      }
+    for (int d = lane; d < D.dim; d += 32) nxt[d] = pop[(size_t)bi * D.dim + d];
+    if (lane == 0) ne[0] = be;
+  }
+  const uint64_t key = run_key(D, run);
+  const uint64_t base = (uint64_t)D.P * D.dim + ((uint64_t)gen * D.off + i) * (uint64_t)(4 + 3 * D.dim);
+  const int ia = (int)(draw_u64(key, base + 1) % (uint64_t)D.P);
+  const int ja = (int)(draw_u64(key, base + 2) % (uint64_t)D.P);
+  const int a = pe[ia] <= pe[ja] ? ia : ja;
+  const int ib = (int)(draw_u64(key, base + 3) % (uint64_t)D.P);
+  const int jb = (int)(draw_u64(key, base + 4) % (uint64_t)D.P);
+  const int b = pe[ib] <= pe[jb] ? ib : jb;
+  for (int d = lane; d < D.dim; d += 32) {
+    const double lam = draw_unit(key, base + 5 + d);
+    double x = lam * pop[(size_t)a * D.dim + d] + (1.0 - lam) * pop[(size_t)b * D.dim + d];
+    x = x + D.sigma * draw_normal(key, base + 5 + D.dim + 2 * (uint64_t)d);
+    if (d >= 3) x = wrap_angle(x);
+    w.g[d] = x;
+    nxt[(size_t)(1 + i) * D.dim + d] = x;
+  }
+  __syncwarp();
+  Frame f;
+  const ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
+  if (lane == 0) ne[1 + i] = (double)o.sums[0];
+}
+
+// Lamarckian step: the r-th best offspring (stable by index) refined by a
+// device-resident local search (docking.cpp:476-489).
+template <int METHOD, int PAIR>
+__global__ void lga_ls_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (item >= D.R * D.L) return;
+  const int run = item / D.L, r = item % D.L;
+  if (!D.active[run]) return;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const int c = D.cur[run];
+  const double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
+  // rank of offspring j (1..off) by (energy, index); pick rank r
+  int target = -1;
+  for (int j = 1 + lane; j <= D.off; j += 32) {
+    const double ej = ne[j];
+    int rank = 0;
+    for (int k = 1; k <= D.off; ++k) {
+      const double ek = ne[k];
+      rank += (ek < ej) || (ek == ej && k < j);
+    }
+    if (rank == r) target = j;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) target = max(target, __shfl_xor_sync(kFull, target, off));
+  const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
+  const LsResult res = local_search_warp<METHOD, PAIR>(S, start, D.ls_iters, D.tol, D.partition,
+                                                       D.half_mode != 0, w);
+  const size_t o = (size_t)run * D.L + r;
+  for (int d = lane; d < D.dim; d += 32) D.lsg[o * D.dim + d] = w.best[d];
+  if (lane == 0) {
+    D.lse[o] = res.energy;
+    D.lsit[o] = res.iterations;
+    D.lscv[o] = res.converged;
+    D.lstarget[o] = target;
+    if (res.status != MDR_OK) D.status[run] = res.status;
+  }
+}
+
+__device__ __forceinline__ void push_record(const LgaDev& D, int run, double e, int it, int cv) {
+  const int k = D.nrec[run];
+  if (k < D.maxrec) {
+    mdr_ls_record rec;
+    rec.best_energy = e;
+    rec.iterations = it;
+    rec.converged = cv;
+    D.recs[(size_t)run * D.maxrec + k] = rec;
+  }
+  D.nrec[run] = k + 1;
+}
+
+// Sequential bookkeeping of one generation, in the reference's order:
+// track_best over offspring 1..off, then LS write-back / track / record in
+// rank order; swap populations; budget test for the next generation.
+__global__ void lga_gen_finalize(LgaDev D, int gen) {
+  const int run = blockIdx.x * blockDim.x + threadIdx.x;
+  if (run >= D.R || !D.active[run]) return;
+  const int c = D.cur[run];
+  double* nxt = D.pop[c ^ 1] + (size_t)run * D.P * D.dim;
+  double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
+  for (int i = 1; i <= D.off; ++i) track_best(D, run, nxt + (size_t)i * D.dim, ne[i]);
+  long long evals = D.evals[run] + D.off;
+  for (int r = 0; r < D.L; ++r) {
+    const size_t o = (size_t)run * D.L + r;
+    const int t = D.lstarget[o];
+    for (int d = 0; d < D.dim; ++d) nxt[(size_t)t * D.dim + d] = D.lsg[o * D.dim + d];
+    ne[t] = D.lse[o];
+    evals += D.lsit[o] + 1;
+    track_best(D, run, D.lsg + o * D.dim, D.lse[o]);
+    push_record(D, run, D.lse[o], D.lsit[o], D.lscv[o]);
+  }
+  D.evals[run] = evals;
+  D.cur[run] = c ^ 1;
+  D.active[run] = (gen + 1 < D.gens) && D.status[run] == MDR_OK && budget_ok(D, evals);
+}
+
+// Final polish from the incumbent best (docking.cpp:501-515), warp per run.
+template <int METHOD, int PAIR>
+__global__ void lga_polish_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int run = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (run >= D.R || D.status[run] != MDR_OK) return;
+  const long long remaining = D.max_evals - D.evals[run];
+  if (remaining <= 1) {
+    if (lane == 0) D.conv[run] = 0;
+    return;
+  }
+  const int iters = (int)((long long)D.ls_iters < remaining - 1 ? (long long)D.ls_iters : remaining - 1);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  const LsResult res = local_search_warp<METHOD, PAIR>(S, D.best_g + (size_t)run * D.dim, iters, D.tol,
+                                                       D.partition, D.half_mode != 0, w);
+  if (lane == 0) {
+    if (res.status != MDR_OK) {
+      D.status[run] = res.status;
+      return;
+    }
+    D.evals[run] += res.iterations + 1;
+    track_best(D, run, w.best, res.energy);
+    push_record(D, run, res.energy, res.iterations, res.converged);
+    D.conv[run] = res.converged;
+  }
+}
+
+__global__ void lga_total_evals(LgaDev D, long long* out) {
+  long long s = 0;
+  for (int r = threadIdx.x; r < D.R; r += blockDim.x) s += D.evals[r];
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  __shared__ long long part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    *out = t;
+  }
+}
+
+// ------------------------------------------------------------ host side
+static size_t warp_smem(const LigandView& L, int wpb) { return ligand_smem_bytes(L) + (size_t)wpb * kWarpRegion; }
+
+template <class K>
+static cudaError_t prep(K kernel, size_t smem) {
+  if (smem > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+#define MDR_DISPATCH(METHOD_VAR, PAIR_VAR, KERNEL, ...)                                        \
+  do {                                                                                         \
+    if (METHOD_VAR == MDR_METHOD_BASELINE && PAIR_VAR == MDR_PAIR_FP64)                        \
+      KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64> __VA_ARGS__;                                  \
+    else if (METHOD_VAR == MDR_METHOD_TCU && PAIR_VAR == MDR_PAIR_FP64)                        \
+      KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64> __VA_ARGS__;                                       \
+    else if (METHOD_VAR == MDR_METHOD_TCU_SPLIT && PAIR_VAR == MDR_PAIR_FP64)                  \
+      KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64> __VA_ARGS__;                                 \
+    else if (METHOD_VAR == MDR_METHOD_BASELINE)                                                \
+      KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32> __VA_ARGS__;                                  \
+    else if (METHOD_VAR == MDR_METHOD_TCU)                                                     \
+      KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32> __VA_ARGS__;                                       \
+    else                                                                                       \
+      KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32> __VA_ARGS__;                                 \
+  } while (0)
+
+#define MDR_PREP(METHOD_VAR, PAIR_VAR, KERNEL, SMEM, ERR)                                      \
+  do {                                                                                         \
+    if (METHOD_VAR == MDR_METHOD_BASELINE && PAIR_VAR == MDR_PAIR_FP64)                        \
+      ERR = prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64>, SMEM);                            \
+    else if (METHOD_VAR == MDR_METHOD_TCU && PAIR_VAR == MDR_PAIR_FP64)                        \
+      ERR = prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64>, SMEM);                                 \
+    else if (METHOD_VAR == MDR_METHOD_TCU_SPLIT && PAIR_VAR == MDR_PAIR_FP64)                  \
+      ERR = prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64>, SMEM);                           \
+    else if (METHOD_VAR == MDR_METHOD_BASELINE)                                                \
+      ERR = prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32>, SMEM);                            \
+    else if (METHOD_VAR == MDR_METHOD_TCU)                                                     \
+      ERR = prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32>, SMEM);                                 \
+    else                                                                                       \
+      ERR = prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32>, SMEM);                           \
+  } while (0)
+
+static inline int blocks_for(long long items, int wpb) { return (int)((items + wpb - 1) / wpb); }
+
+cudaError_t launch_score(const LigandView& L, const double* genos, int n, int method, int pair, int partition,
+                         int half_mode, float* energy, float* grad, float* torque, cudaStream_t s, int wpb) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = warp_smem(L, wpb);
+  cudaError_t e = cudaSuccess;
+  MDR_PREP(method, pair, score_kernel, smem, e);
+  if (e != cudaSuccess) return e;
+  MDR_DISPATCH(method, pair, score_kernel,
+               <<<blocks_for(n, wpb), 32 * wpb, smem, s>>>(L, genos, n, partition, half_mode, energy, grad, torque));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_score_reference(const LigandView& L, const double* genos, int n, double* energy, double* grad,
+                                   double* torque, cudaStream_t s, int wpb) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = warp_smem(L, wpb);
+  cudaError_t e = prep(scoreref_kernel, smem);
+  if (e != cudaSuccess) return e;
+  scoreref_kernel<<<blocks_for(n, wpb), 32 * wpb, smem, s>>>(L, genos, n, energy, grad, torque);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adadelta(int dim, int n, double rho, double eps, double* sq_g, double* sq_u, double* geno,
+                            const double* grad, int* status, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  adadelta_kernel<<<blocks_for(n, 4), 128, 0, s>>>(dim, n, rho, eps, sq_g, sq_u, geno, grad, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_local_search(const LigandView& L, const double* starts, int n, int max_iters, double tol,
+                                int method, int pair, int partition, int half_mode, double* out_g, double* out_e,
+                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb) {
+  if (n <= 0) return cudaSuccess;
+  const size_t smem = warp_smem(L, wpb);
+  cudaError_t e = cudaSuccess;
+  MDR_PREP(method, pair, ls_kernel, smem, e);
+  if (e != cudaSuccess) return e;
+  MDR_DISPATCH(method, pair, ls_kernel,
+               <<<blocks_for(n, wpb), 32 * wpb, smem, s>>>(L, starts, n, max_iters, tol, partition, half_mode,
+                                                           out_g, out_e, out_it, out_cv, status));
+  return cudaGetLastError();
+}
+
+cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb) {
+  const size_t smem = warp_smem(L, wpb);
+  cudaError_t e = cudaSuccess;
+  MDR_PREP(method, pair, lga_init_kernel, smem, e);
+  if (e == cudaSuccess) MDR_PREP(method, pair, lga_offspring_kernel, smem, e);
+  if (e == cudaSuccess) MDR_PREP(method, pair, lga_ls_kernel, smem, e);
+  if (e == cudaSuccess) MDR_PREP(method, pair, lga_polish_kernel, smem, e);
+  return e;
+}
+
+// Enqueue a whole docking batch; prepare_lga() must have run (it is not
+// capture-safe, launch_lga is).
+cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
+                       int* n_launches) {
+  const size_t smem = warp_smem(L, wpb);
+  int launches = 0;
+  MDR_DISPATCH(method, pair, lga_init_kernel, <<<blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s>>>(L, D));
+  lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
+  launches += 2;
+  for (int gen = 0; gen < D.gens; ++gen) {
+    MDR_DISPATCH(method, pair, lga_offspring_kernel,
+                 <<<blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s>>>(L, D, gen));
+    if (D.L > 0)
+      MDR_DISPATCH(method, pair, lga_ls_kernel, <<<blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s>>>(L, D));
+    lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
+    launches += D.L > 0 ? 3 : 2;
+  }
+  MDR_DISPATCH(method, pair, lga_polish_kernel, <<<blocks_for(D.R, wpb), 32 * wpb, smem, s>>>(L, D));
+  launches += 1;
+  if (n_launches) *n_launches = launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s) {
+  lga_total_evals<<<1, 256, 0, s>>>(D, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mdr

@@ -1,0 +1,38 @@
+// dock_launch.h — host-callable launchers of the CUDA kernels (no CUDA types
+// leak past capi.cpp; the public boundary is include/mdr.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "mdr_shared.h"
+
+namespace mdr {
+
+// dock.cu
+cudaError_t launch_score(const LigandView& L, const double* genos, int n, int method, int pair, int partition,
+                         int half_mode, float* energy, float* grad, float* torque, cudaStream_t s, int wpb);
+cudaError_t launch_score_reference(const LigandView& L, const double* genos, int n, double* energy, double* grad,
+                                   double* torque, cudaStream_t s, int wpb);
+cudaError_t launch_adadelta(int dim, int n, double rho, double eps, double* sq_g, double* sq_u, double* geno,
+                            const double* grad, int* status, cudaStream_t s);
+cudaError_t launch_local_search(const LigandView& L, const double* starts, int n, int max_iters, double tol,
+                                int method, int pair, int partition, int half_mode, double* out_g, double* out_e,
+                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb);
+cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb);
+cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
+                       int* n_launches);
+cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s);
+
+// reduce.cu
+cudaError_t launch_f32_to_half(const float* in, size_t n, uint16_t* out, cudaStream_t s);
+cudaError_t launch_half_to_f32(const uint16_t* in, size_t n, float* out, cudaStream_t s);
+cudaError_t launch_mma16(const uint16_t* a, const uint16_t* b, const float* c, int n_tiles, int half_mode, float* d,
+                         cudaStream_t s);
+cudaError_t launch_warp_reduce(const float* lanes, int n_red, float* out, cudaStream_t s);
+cudaError_t launch_block_reduce(const float* values, int threads, int n_red, float* out, cudaStream_t s);
+cudaError_t launch_reduce4(const float* vecs, int n, int n_red, int method, int half_mode, float* out,
+                           cudaStream_t s);
+cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int half_mode, float* out,
+                           cudaStream_t s);
+
+}  // namespace mdr

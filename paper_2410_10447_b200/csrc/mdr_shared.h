@@ -1,0 +1,64 @@
+// mdr_shared.h — plain structs shared by host (capi.cpp) and device code.
+#pragma once
+
+#include <stdint.h>
+
+#include "mdr.h"
+
+#include <vector_types.h>  // double4 / float4 / float2 for host and device
+
+namespace mdr {
+
+// Limits of the device path (documented in DESIGN.md; validated by capi.cpp
+// before any launch, reported as MDR_ERR_SIZE).
+constexpr int kMaxDim = 64;        // genotype dimensions: lanes d and d + 32
+constexpr int kMaxRot = kMaxDim - 6;
+constexpr int kMaxSites = 2048;    // per-CTA shared-memory copy
+constexpr int kMaxAtoms = 4096;
+constexpr int kWindow = 16;        // local_search convergence window, docking.cpp:314
+
+// One receptor site with the two pair-loop constants precomputed on the host
+// in the reference's evaluation order (docking.cpp:114-116):
+//   c2 = 0.5625 * d0 * d0 ; num = d0 * d0 + c2.
+struct SiteD {
+  double x, y, z, depth, c2, num;
+};
+
+// Device view of an uploaded ligand / receptor pair.
+struct LigandView {
+  int n_atoms, n_sites, n_rot, pad;
+  const SiteD* sites;
+  const double4* atoms;  // local x, y, z, weight
+  const int* tors;
+  const double* taxes;      // torsion_axis(k) computed on the host (glibc)
+  const float4* sites_f;    // fast-mode copy: x, y, z, depth
+  const float2* sites_f2;   // fast-mode copy: c2, num
+  double box_lo[3], box_hi[3];  // random_genotype bounds incl. margin
+};
+
+// All device state of a batch of LGA runs (docking.cpp:392-517).
+struct LgaDev {
+  int R, P, dim, off, L, gens, ls_iters, maxrec, partition, half_mode;
+  long long max_evals;
+  double tol, sigma;
+  uint64_t label_hash;  // mix64(fnv1a64("lga")), rng.cpp:31-32
+  const uint64_t* seeds;
+  double* pop[2];   // [R][P][dim]
+  double* pope[2];  // [R][P]
+  int* cur;         // [R]
+  double* lsg;      // [R][L][dim]
+  double* lse;      // [R][L]
+  int* lsit;        // [R][L]
+  int* lscv;        // [R][L]
+  int* lstarget;    // [R][L]
+  double* best_e;   // [R]
+  double* best_g;   // [R][dim]
+  long long* evals; // [R]
+  int* active;      // [R]
+  int* nrec;        // [R]
+  mdr_ls_record* recs;  // [R][maxrec]
+  int* conv;        // [R]
+  int* status;      // [R]
+};
+
+}  // namespace mdr

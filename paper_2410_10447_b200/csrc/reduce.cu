@@ -1,0 +1,260 @@
+// reduce.cu — L0/L1 units behind the reduce.hpp / mma.hpp / half.hpp API:
+// binary16 conversions, the 16x16x16 MMA unit on tensor cores, and batched
+// warp / block / reduce4 / reduce7 reductions (one warp per reduction; the
+// reference's simulated block of B threads is B/32 register groups of one
+// warp, so Baseline results are bit-identical to reduce.cpp and Tcu results
+// follow the reference's packing and AccumMode rounding on real mma.sync).
+// Compiled with --fmad=false.
+#include <cuda_runtime.h>
+
+#include "dock_launch.h"
+#include "mdr_device.cuh"
+
+namespace mdr {
+
+// ------------------------------------------------------------- binary16
+// f32_to_half half.cpp:8-54: cvt.rn.f16.f32 is RNE with subnormals kept and
+// overflow to inf; NaNs are canonicalised to 0x7E00 like the reference.
+__global__ void f32_to_half_kernel(const float* __restrict__ in, size_t n, uint16_t* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    out[i] = isnan(v) ? (uint16_t)0x7E00u : __half_as_ushort(__float2half_rn(v));
+  }
+}
+
+// half_to_f32 half.cpp:56-74: exact widening, NaN -> 0x7FC00000.
+__global__ void half_to_f32_kernel(const uint16_t* __restrict__ in, size_t n, float* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint16_t h = in[i];
+    const bool nan = (h & 0x7C00u) == 0x7C00u && (h & 0x3FFu);
+    out[i] = nan ? __uint_as_float(0x7FC00000u) : __half2float(__ushort_as_half(h));
+  }
+}
+
+// ------------------------------------------------------------- MMA unit
+// mma mma.cpp:41-64: D = A*B + C for one 16x16x16 tile per warp, as two
+// m16n8k16 f16 x f16 -> f32 tensor-core ops; Half mode rounds D once.
+__global__ void mma16_kernel(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B,
+                             const float* __restrict__ Cm, int n_tiles, int half_mode, float* __restrict__ Dm) {
+  const int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tile >= n_tiles) return;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const uint16_t* a = A + (size_t)tile * 256;
+  const uint16_t* b = B + (size_t)tile * 256;
+  const float* c = Cm + (size_t)tile * 256;
+  float* d = Dm + (size_t)tile * 256;
+  auto pair = [](uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); };
+  const uint32_t af[4] = {pair(a[g * 16 + 2 * t], a[g * 16 + 2 * t + 1]),
+                          pair(a[(g + 8) * 16 + 2 * t], a[(g + 8) * 16 + 2 * t + 1]),
+                          pair(a[g * 16 + 2 * t + 8], a[g * 16 + 2 * t + 9]),
+                          pair(a[(g + 8) * 16 + 2 * t + 8], a[(g + 8) * 16 + 2 * t + 9])};
+#pragma unroll
+  for (int nb = 0; nb < 2; ++nb) {
+    const int col = 8 * nb + g;
+    const uint32_t b0 = pair(b[(2 * t) * 16 + col], b[(2 * t + 1) * 16 + col]);
+    const uint32_t b1 = pair(b[(2 * t + 8) * 16 + col], b[(2 * t + 9) * 16 + col]);
+    const int c0 = 8 * nb + 2 * t;
+    const float cf[4] = {c[g * 16 + c0], c[g * 16 + c0 + 1], c[(g + 8) * 16 + c0], c[(g + 8) * 16 + c0 + 1]};
+    float df[4];
+    mma_f16_16816(df, af, b0, b1, cf);
+    if (half_mode)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) df[q] = hround(df[q]);
+    d[g * 16 + c0] = df[0];
+    d[g * 16 + c0 + 1] = df[1];
+    d[(g + 8) * 16 + c0] = df[2];
+    d[(g + 8) * 16 + c0 + 1] = df[3];
+  }
+}
+
+// ------------------------------------------------------------ reductions
+__global__ void warp_reduce_kernel(const float* __restrict__ lanes, int n_red, float* __restrict__ out) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_red) return;
+  const int lane = threadIdx.x & 31;
+  const float s = warp_tree(lanes[(size_t)r * 32 + lane]);
+  if (lane == 0) out[r] = s;
+}
+
+// baseline_block_reduce reduce.cpp:136-163: warp totals added to a zero
+// accumulator in ascending warp order — in registers of one warp.
+__global__ void block_reduce_kernel(const float* __restrict__ values, int threads, int n_red,
+                                    float* __restrict__ out) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n_red) return;
+  const int lane = threadIdx.x & 31;
+  const float* v = values + (size_t)r * threads;
+  float acc = 0.0f;
+  for (int w = 0; w < threads / 32; ++w) acc = acc + warp_tree(v[32 * w + lane]);
+  if (lane == 0) out[r] = acc;
+}
+
+constexpr int kRedWarps = 4;
+
+template <int METHOD>
+__global__ void reduce4_kernel(const float4* __restrict__ vecs, int n, int n_red, int half_mode,
+                               float4* __restrict__ out) {
+  __shared__ __align__(16) unsigned char scratch[kRedWarps][kWarpScratchBytes];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kRedWarps + warp;
+  if (r >= n_red) return;
+  const float4* v = vecs + (size_t)r * n;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (METHOD == MDR_METHOD_TCU) {
+    __half* tile = reinterpret_cast<__half*>(scratch[warp]);
+    float V[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n; c += 64) {
+      const float4 v0 = c + lane < n ? v[c + lane] : z;
+      const float4 v1 = c + 32 + lane < n ? v[c + 32 + lane] : z;
+      tcu_tile(V, v0, v1, tile, half_mode != 0, lane);
+    }
+    const float w = tcu_q_step(V, half_mode != 0, lane);
+    const float x = __shfl_sync(kFull, w, 0), y = __shfl_sync(kFull, w, 4);
+    const float zz = __shfl_sync(kFull, w, 8), e = __shfl_sync(kFull, w, 12);
+    if (lane == 0) out[r] = make_float4(x, y, zz, e);
+  } else if (METHOD == MDR_METHOD_TCU_SPLIT) {
+    float* stage = reinterpret_cast<float*>(scratch[warp] + 2 * 256 * 2);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n; c += 32) {
+      const float4 q = c + lane < n ? v[c + lane] : z;
+      const float rec[7] = {q.x, q.y, q.z, q.w, 0.f, 0.f, 0.f};
+      split_group(acc, rec, stage, lane);
+    }
+    const float tot = acc[0] + acc[2];
+    const float x = __shfl_sync(kFull, tot, 0), y = __shfl_sync(kFull, tot, 4);
+    const float zz = __shfl_sync(kFull, tot, 8), e = __shfl_sync(kFull, tot, 12);
+    if (lane == 0) out[r] = make_float4(x, y, zz, e);
+  } else {  // simulate_block baseline: four sequential block reductions
+    float ax = 0.f, ay = 0.f, az = 0.f, ae = 0.f;
+    for (int w = 0; w < n; w += 32) {
+      const float4 q = v[w + lane];
+      ax = ax + warp_tree(q.x);
+      ay = ay + warp_tree(q.y);
+      az = az + warp_tree(q.z);
+      ae = ae + warp_tree(q.w);
+    }
+    if (lane == 0) out[r] = make_float4(ax, ay, az, ae);
+  }
+}
+
+template <int METHOD>
+__global__ void reduce7_kernel(const float* __restrict__ recs, int n, int n_red, int half_mode,
+                               float* __restrict__ out) {
+  __shared__ __align__(16) unsigned char scratch[kRedWarps][kWarpScratchBytes];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kRedWarps + warp;
+  if (r >= n_red) return;
+  const float* base = recs + (size_t)r * n * 7;
+  auto load = [&](int j, float (&q)[7]) {
+#pragma unroll
+    for (int c = 0; c < 7; ++c) q[c] = j < n ? base[(size_t)j * 7 + c] : 0.f;
+  };
+  float s[7];
+  if (METHOD == MDR_METHOD_BASELINE) {
+#pragma unroll
+    for (int c = 0; c < 7; ++c) s[c] = 0.f;
+    for (int w = 0; w < n; w += 32) {
+      float q[7];
+      load(w + lane, q);
+#pragma unroll
+      for (int c = 0; c < 7; ++c) s[c] = s[c] + warp_tree(q[c]);
+    }
+  } else if (METHOD == MDR_METHOD_TCU) {
+    __half* tile = reinterpret_cast<__half*>(scratch[warp]);
+    float vg[4] = {0.f, 0.f, 0.f, 0.f}, vt[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n; c += 64) {
+      float a[7], b[7];
+      load(c + lane, a);
+      load(c + 32 + lane, b);
+      tcu_tile(vg, make_float4(a[1], a[2], a[3], a[0]), make_float4(b[1], b[2], b[3], b[0]), tile,
+               half_mode != 0, lane);
+      tcu_tile(vt, make_float4(a[4], a[5], a[6], 0.f), make_float4(b[4], b[5], b[6], 0.f), tile + 256,
+               half_mode != 0, lane);
+    }
+    const float wg = tcu_q_step(vg, half_mode != 0, lane);
+    const float wt = tcu_q_step(vt, half_mode != 0, lane);
+    s[0] = __shfl_sync(kFull, wg, 12);
+    s[1] = __shfl_sync(kFull, wg, 0);
+    s[2] = __shfl_sync(kFull, wg, 4);
+    s[3] = __shfl_sync(kFull, wg, 8);
+    s[4] = __shfl_sync(kFull, wt, 0);
+    s[5] = __shfl_sync(kFull, wt, 4);
+    s[6] = __shfl_sync(kFull, wt, 8);
+  } else {
+    float* stage = reinterpret_cast<float*>(scratch[warp] + 2 * 256 * 2);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < n; c += 32) {
+      float q[7];
+      load(c + lane, q);
+      split_group(acc, q, stage, lane);
+    }
+    const float tot = acc[0] + acc[2];
+#pragma unroll
+    for (int c = 0; c < 7; ++c) s[c] = __shfl_sync(kFull, tot, 4 * c);
+  }
+  if (lane < 7) {
+    float v = s[0];
+#pragma unroll
+    for (int c = 1; c < 7; ++c) v = lane == c ? s[c] : v;
+    out[(size_t)r * 7 + lane] = v;
+  }
+}
+
+// ------------------------------------------------------------ launchers
+static int grid_for(size_t n, int block) {
+  size_t g = (n + block - 1) / block;
+  return (int)(g > 148 * 16 ? 148 * 16 : (g == 0 ? 1 : g));
+}
+
+cudaError_t launch_f32_to_half(const float* in, size_t n, uint16_t* out, cudaStream_t s) {
+  f32_to_half_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_half_to_f32(const uint16_t* in, size_t n, float* out, cudaStream_t s) {
+  half_to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_mma16(const uint16_t* a, const uint16_t* b, const float* c, int n_tiles, int half_mode, float* d,
+                         cudaStream_t s) {
+  if (n_tiles <= 0) return cudaSuccess;
+  mma16_kernel<<<(n_tiles + 3) / 4, 128, 0, s>>>(a, b, c, n_tiles, half_mode, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_warp_reduce(const float* lanes, int n_red, float* out, cudaStream_t s) {
+  if (n_red <= 0) return cudaSuccess;
+  warp_reduce_kernel<<<(n_red + 3) / 4, 128, 0, s>>>(lanes, n_red, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_block_reduce(const float* values, int threads, int n_red, float* out, cudaStream_t s) {
+  if (n_red <= 0) return cudaSuccess;
+  block_reduce_kernel<<<(n_red + 3) / 4, 128, 0, s>>>(values, threads, n_red, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce4(const float* vecs, int n, int n_red, int method, int half_mode, float* out,
+                           cudaStream_t s) {
+  if (n_red <= 0) return cudaSuccess;
+  const int grid = (n_red + kRedWarps - 1) / kRedWarps;
+  const float4* v = reinterpret_cast<const float4*>(vecs);
+  float4* o = reinterpret_cast<float4*>(out);
+  if (method == MDR_METHOD_TCU)
+    reduce4_kernel<MDR_METHOD_TCU><<<grid, 32 * kRedWarps, 0, s>>>(v, n, n_red, half_mode, o);
+  else if (method == MDR_METHOD_TCU_SPLIT)
+    reduce4_kernel<MDR_METHOD_TCU_SPLIT><<<grid, 32 * kRedWarps, 0, s>>>(v, n, n_red, half_mode, o);
+  else
+    reduce4_kernel<MDR_METHOD_BASELINE><<<grid, 32 * kRedWarps, 0, s>>>(v, n, n_red, half_mode, o);
+  return cudaGetLastError();
+}
+cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int half_mode, float* out,
+                           cudaStream_t s) {
+  if (n_red <= 0) return cudaSuccess;
+  const int grid = (n_red + kRedWarps - 1) / kRedWarps;
+  if (method == MDR_METHOD_TCU)
+    reduce7_kernel<MDR_METHOD_TCU><<<grid, 32 * kRedWarps, 0, s>>>(recs, n, n_red, half_mode, out);
+  else if (method == MDR_METHOD_TCU_SPLIT)
+    reduce7_kernel<MDR_METHOD_TCU_SPLIT><<<grid, 32 * kRedWarps, 0, s>>>(recs, n, n_red, half_mode, out);
+  else
+    reduce7_kernel<MDR_METHOD_BASELINE><<<grid, 32 * kRedWarps, 0, s>>>(recs, n, n_red, half_mode, out);
+  return cudaGetLastError();
+}
+
+}  // namespace mdr

@@ -1,0 +1,253 @@
+"""GPU parity of scoring, ADADELTA, local search and LGA (C-ABI) against the
+CPU oracle and the fixtures recorded from the reference itself.
+
+Tolerances (written here):
+  * Baseline method with FP64 pair terms (the default): per-evaluation float
+    outputs bit-identical to the reference for >= 99 % of poses; the rest
+    (a CUDA sin/cos differing from glibc by an ulp) within 1e-6 relative.
+  * Tcu method (paper's f16 MMA): per-component within 2 half-ulps of the
+    reference's emulated result (hardware fp32 accumulation order).
+  * TcuSplit and the FP32 fast pair mode: energy within 1e-4 * max(|E|, 1) and
+    gradient within 1e-4 * max(max|g|, 1) of the fp32 reference (Baseline).
+  * Full LGA runs: statistical parity (paired seeds, relative difference of
+    mean best energies < 0.2 %, the reference's acceptance.cpp:128-145 gate);
+    plus exact equality of runs whose trajectories do not diverge.
+"""
+import numpy as np
+import pytest
+
+from paper_2410_10447_b200 import (
+    BASELINE,
+    HALF,
+    PAIR_FP32,
+    PAIR_FP64,
+    SINGLE,
+    TCU,
+    TCU_SPLIT,
+    Device,
+    LgaSettings,
+    NumericDomainError,
+    SizeError,
+    UnsupportedBlockSizeError,
+    validate_pair,
+)
+from paper_2410_10447_b200._abi import Instance, derive_rng, random_instance, random_pose
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(x):
+    return np.asarray(x, np.float32).view(np.uint32)
+
+
+def half_ulp(v):
+    a = np.maximum(np.abs(np.asarray(v, np.float64)), 2.0**-14)
+    return 2.0 ** (np.floor(np.log2(a)) - 10)
+
+
+def random_cases(seed, count, natoms_max=40, nsites_max=40):
+    rng = derive_rng(seed, "gpu/score")
+    out = []
+    for rep in range(count):
+        inst = random_instance(rng, rep % 9, 1 + rng.next_index(natoms_max), 1 + rng.next_index(nsites_max))
+        poses = np.stack([random_pose(rng, inst.n_rot, 1.0 if k % 2 else 0.4) for k in range(16)])
+        out.append((inst, poses))
+    return out
+
+
+def test_score_golden_fixtures(dev, instances, ref_vectors):
+    mism = 0
+    total = 0
+    for c in ref_vectors["score"]:
+        if c["method"] == "reference":
+            continue
+        inst = instances[c["inst"]]
+        r = dev.score(inst, np.array(c["g"]), c["method"], c["accum"], c["partition"])
+        assert list(r.reduce_stats.as_tuple()) == c["stats"]
+        want_e, want_g = np.float32(c["energy"]), np.array(c["grad"], np.float32)
+        if c["method"] == BASELINE:
+            total += 1
+            same = bits(r.energy) == bits(want_e) and np.array_equal(bits(r.gradient), bits(want_g))
+            mism += not same
+            assert abs(float(r.energy) - float(want_e)) <= 1e-6 * max(abs(float(want_e)), 1.0)
+        else:
+            assert abs(float(r.energy) - float(want_e)) <= 2 * half_ulp(want_e)
+    assert mism <= 0.01 * total + 1
+
+
+def test_score_stationary_single_well(dev):
+    inst = Instance(np.array([[1.5, 0, 0, 1.0]]), np.array([-1]), np.array([[0, 0, 0, 1.25, 1.5]]), 0)
+    for m, a in ((BASELINE, SINGLE), (TCU, SINGLE), (TCU, HALF), (TCU_SPLIT, SINGLE)):
+        r = dev.score(inst, np.zeros(6), m, a, 64)
+        assert r.energy == np.float32(-1.25) and not r.gradient.any() and not r.torque.any()
+
+
+def test_score_validation(dev, instances):
+    inst = instances["s1"]
+    with pytest.raises(UnsupportedBlockSizeError):
+        dev.score(inst, np.zeros(6), TCU, HALF, 32)
+    with pytest.raises(UnsupportedBlockSizeError):
+        dev.score(inst, np.zeros(6), BASELINE, HALF, 48)
+    with pytest.raises(SizeError):
+        dev.score(inst, np.zeros(8), BASELINE, HALF, 64)
+    dev.score(inst, np.zeros(6), BASELINE, SINGLE, 32)
+
+
+@pytest.mark.parametrize("partition", [32, 64, 128])
+def test_score_baseline_bit_exact_random(dev, port, partition):
+    exact = total = 0
+    for inst, poses in random_cases(100 + partition, 25, natoms_max=140):
+        e, g, t, _ = dev.score_batch(inst, poses, BASELINE, SINGLE, partition)
+        for i, p in enumerate(poses):
+            we, wg, wt, _ = port.score(inst, p, BASELINE, SINGLE, partition)
+            total += 1
+            same = bits(e[i]) == bits(we) and np.array_equal(bits(g[i]), bits(wg)) and np.array_equal(
+                bits(t[i]), bits(wt))
+            exact += same
+            scale = max(float(np.abs(wg).max()), 1.0)
+            assert abs(float(e[i]) - float(we)) <= 1e-6 * max(abs(float(we)), 1.0)
+            assert np.abs(g[i] - wg).max() <= 1e-6 * scale
+    assert exact >= 0.99 * total, (exact, total)
+
+
+def test_score_tcu_reference_compatible(dev, port):
+    for inst, poses in random_cases(7, 10):
+        for mode in (HALF, SINGLE):
+            e, g, t, st = dev.score_batch(inst, poses, TCU, mode, 64)
+            for i, p in enumerate(poses):
+                we, wg, wt, wst = port.score(inst, p, TCU, mode, 64)
+                assert st == wst
+                assert abs(float(e[i]) - float(we)) <= 2 * half_ulp(we)
+                assert np.all(np.abs(t[i] - wt) <= 2 * half_ulp(wt))
+
+
+@pytest.mark.parametrize("method,pair", [(TCU_SPLIT, PAIR_FP64), (BASELINE, PAIR_FP32), (TCU_SPLIT, PAIR_FP32)])
+def test_score_within_1e4_of_fp32_reference(method, pair, port, dev):
+    dev = Device(0, pair=pair)
+    worst_e = worst_g = 0.0
+    for inst, poses in random_cases(31, 20, natoms_max=100, nsites_max=64):
+        e, g, _, _ = dev.score_batch(inst, poses, method, SINGLE, 128)
+        for i, p in enumerate(poses):
+            we, wg, _, _ = port.score(inst, p, BASELINE, SINGLE, 128)
+            worst_e = max(worst_e, abs(float(e[i]) - float(we)) / max(abs(float(we)), 1.0))
+            worst_g = max(worst_g, float(np.abs(g[i] - wg).max()) / max(float(np.abs(wg).max()), 1.0))
+    dev.close()
+    assert worst_e <= 1e-4 and worst_g <= 1e-4, (worst_e, worst_g)
+
+
+def test_score_reference_and_fd(dev, port):
+    for inst, poses in random_cases(55, 10):
+        e, g, t = dev.score_reference_batch(inst, poses)
+        for i, p in enumerate(poses):
+            we, wg, wt = port.score_reference(inst, p)
+            assert abs(e[i] - we) <= 1e-12 * max(abs(we), 1.0)
+            assert np.abs(g[i] - wg).max() <= 1e-12 * max(np.abs(wg).max(), 1.0)
+
+
+def test_adadelta_step_bit_exact(dev, port):
+    rng = np.random.default_rng(5)
+    n, dim = 64, 14
+    a = [rng.uniform(0, 1, (n, dim)), rng.uniform(0, 1e-3, (n, dim)), rng.uniform(-4, 4, (n, dim)),
+         rng.normal(size=(n, dim))]
+    got = dev.adadelta_step_batch(*a)
+    for i in range(n):
+        want = port.adadelta_step(a[0][i], a[1][i], a[2][i], a[3][i])
+        for u, v in zip(got, want):
+            assert np.array_equal(u[i], v)
+    sg, su, g = dev.adadelta_step(np.zeros(6), np.zeros(6), np.zeros(6), [1, 0, 0, 0, 0, 0])
+    assert abs(g[0] - -0.004472091234310839) <= 1e-12 * 0.0045
+    bad = np.zeros(6)
+    bad[3] = np.nan
+    with pytest.raises(NumericDomainError):
+        dev.adadelta_step(np.zeros(6), np.zeros(6), np.zeros(6), bad)
+
+
+def test_local_search_golden(dev, instances, ref_vectors):
+    exact = total = 0
+    for c in ref_vectors["local_search"]:
+        r = dev.local_search(instances[c["inst"]], np.array(c["start"]), c["max_iters"], c["tol"], c["method"],
+                             c["accum"], 64)
+        if c["method"] == BASELINE:
+            total += 1
+            same = (r.energy == c["energy"] and r.iterations == c["iterations"] and r.converged == c["converged"]
+                    and np.array_equal(r.genotype, np.array(c["genotype"])))
+            exact += same
+            assert abs(r.energy - c["energy"]) <= 1e-5 * max(abs(c["energy"]), 1.0)
+        assert r.stats.block_syncs == (r.iterations + 1) * (21 if c["method"] == BASELINE else 4)
+    assert exact >= total - 1, (exact, total)
+
+
+def test_local_search_single_well(dev):
+    inst = Instance(np.array([[1.5, 0, 0, 1.0]]), np.array([-1]), np.array([[0, 0, 0, 1.25, 1.5]]), 0)
+    ls = dev.local_search(inst, np.zeros(6), 100, 1e-6, TCU, HALF, 64)
+    assert ls.converged and ls.iterations <= 17 and ls.energy == -1.25 and not ls.genotype.any()
+    ls = dev.local_search(inst, np.array([0.9, -0.4, 0.3, 0, 0, 0]), 600, 1e-7, BASELINE, SINGLE, 64)
+    assert abs(ls.energy - -1.25) <= 1.25e-3 and ls.iterations >= 16
+
+
+def test_local_search_batch_vs_oracle(dev, port, instances):
+    inst = instances["s3"]
+    rng = derive_rng(6005, "dock-det")
+    starts = np.stack([random_pose(rng, inst.n_rot, 0.6) for _ in range(64)])
+    res = dev.local_search_batch(inst, starts, 150, 1e-4, BASELINE, SINGLE, 64)
+    same = 0
+    for s, r in zip(starts, res):
+        w = port.local_search(inst, s, 150, 1e-4, BASELINE, SINGLE, 64)
+        same += r.energy == w["energy"] and r.iterations == w["iterations"]
+    assert same >= 60, same
+
+
+def test_lga_golden_and_determinism(dev, instances, ref_vectors):
+    exact = 0
+    for c in ref_vectors["lga_run"]:
+        s = LgaSettings(**c["settings"])
+        r = dev.lga_run(instances[c["inst"]], c["method"], c["accum"], s, c["seed"])
+        assert r.evaluations <= s.max_evaluations
+        assert r.best_energy == min(x[0] for x in r.runs) or r.best_energy <= min(x[0] for x in r.runs)
+        assert list(r.total_stats.as_tuple()) == [r.evaluations * x for x in
+                                                  dev.score(instances[c["inst"]], np.zeros(instances[c["inst"]].dim),
+                                                            c["method"], c["accum"], s.partition).reduce_stats.as_tuple()]
+        if c["method"] == BASELINE:
+            same = (r.best_energy == c["best_energy"] and r.evaluations == c["evaluations"]
+                    and [list(x) for x in r.runs] == [[x[0], x[1], bool(x[2])] for x in c["runs"]])
+            exact += same
+    assert exact >= 3, exact
+    s = LgaSettings()
+    a = dev.lga_run_batch(instances["s2"], TCU, HALF, s, [20260816, 20260816])
+    assert a[0].best_energy == a[1].best_energy and np.array_equal(a[0].best_genotype, a[1].best_genotype)
+    assert a[0].runs == a[1].runs and a[0].evaluations == a[1].evaluations
+
+
+def test_lga_budget_and_degenerate(dev, instances):
+    inst = instances["s1"]
+    r = dev.lga_run(inst, BASELINE, SINGLE, LgaSettings(population_size=6, generations=50, max_evaluations=200,
+                                                         ls_max_iters=40), 7)
+    assert r.evaluations <= 200
+    r = dev.lga_run(inst, BASELINE, SINGLE, LgaSettings(population_size=2, generations=1, mutation_sigma=0.0,
+                                                         ls_fraction=1.0, ls_max_iters=60), 99)
+    assert len(r.runs) == 2 and r.best_energy == min(x[0] for x in r.runs)
+    with pytest.raises(SizeError):
+        dev.lga_run(inst, BASELINE, SINGLE, LgaSettings(population_size=1), 1)
+
+
+@pytest.mark.parametrize("name", ["s1", "s2", "s3"])
+def test_lga_paired_statistical_parity(dev, port, instances, name):
+    """GPU Baseline vs the CPU reference path, 100 paired seeds (acceptance
+    check 3 methodology): relative difference of mean best energies < 0.2 %."""
+    inst = instances[name]
+    s = LgaSettings()
+    seeds = np.arange(100, dtype=np.uint64) + np.uint64(12345)
+    gpu = dev.lga_run_batch(inst, BASELINE, SINGLE, s, seeds)
+    cpu = [port.lga_run(inst, BASELINE, SINGLE, s, int(x)) for x in seeds]
+    mg = np.mean([r.best_energy for r in gpu])
+    mc = np.mean([r["best_energy"] for r in cpu])
+    assert abs(mg - mc) / abs(mc) < 0.002
+    same = sum(g.best_energy == c["best_energy"] and g.evaluations == c["evaluations"] for g, c in zip(gpu, cpu))
+    assert same >= 50, same  # most trajectories are reproduced exactly
+
+
+def test_validate_pair_tcu_vs_baseline(dev, instances):
+    rep = validate_pair(dev, instances["s2"], BASELINE, TCU, HALF, 100, 12345, LgaSettings())
+    assert rep["relative_error"] < 0.002
+    rep = validate_pair(dev, instances["s2"], BASELINE, TCU_SPLIT, SINGLE, 100, 12345, LgaSettings())
+    assert rep["relative_error"] < 0.002
