@@ -210,14 +210,6 @@ extern "C" __global__ void dfma_peak(double* out, int iters) {
   if (a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7 == 1234.5) out[threadIdx.x] = a0;
 }
 """
-    try:
-        from cuda.bindings import nvrtc  # noqa: F401
-    except Exception:
-        pass
-    try:
-        import cupy  # noqa: F401
-    except Exception:
-        pass
     # compile with nvcc once into profiles-independent cache
     cache = os.path.join(ROOT, "paper_2410_10447_b200", "build")
     os.makedirs(cache, exist_ok=True)
@@ -278,7 +270,11 @@ def run_gpu_arm(args):
     lib = load()
     pair = PAIR_FP32 if args.pair == "fp32" else PAIR_FP64
     dev = Device(local, pair=pair, warps_per_block=args.wpb)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream shared by torch and the library, so the
+    # CUDA events below bracket exactly the library's work
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     dev.set_stream(stream.cuda_stream)
     inst = workload()
     settings = LgaSettings()

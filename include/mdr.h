@@ -143,6 +143,18 @@ int mdr_warp_reduce_batch(mdr_ctx* ctx, const float* lanes, int n_red,
 int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red,
                       int method, int accum, float* out, mdr_sync_stats* stats);
 
+/* C2 microbench (no reference counterpart; cli.cpp:195-266 is its CPU
+ * analogue): kernel k in [0, mdr_reduce_bench_kernels()) reduces float4 per
+ * thread over blocks of `block` threads.  chain_steps > 0: n_red/chain_steps
+ * blocks each run a dependent chain of chain_steps reduce-and-broadcast
+ * steps on one input set (d_in: blocks x block x 4 floats); chain_steps == 0:
+ * n_red distinct input sets streamed from HBM.  d_out: one float4 per block
+ * (chain) or per reduction (stream).  Device pointers, enqueue only. */
+int mdr_reduce_bench_kernels(void);
+const char* mdr_reduce_bench_kernel_name(int kernel);
+int mdr_reduce_bench_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in,
+                         int n_red, int chain_steps, float* d_out);
+
 /* ---- L2 scoring (docking.hpp:44-63) ------------------------------------ */
 /* score docking.cpp:191-233 for n genotypes (n x dim, dim = 6 + n_rot,
  * order x,y,z,phi,theta,alpha,torsions).  gradient n x dim, torque n x 3.
@@ -219,6 +231,11 @@ int mdr_lga_batch_download(mdr_ctx* ctx, mdr_lga_batch* b, double* best_energy,
 /* Sum of evaluations over the batch's runs, reduced on the device into a
  * single int64 at d_total (for D2H of one word per step). */
 int mdr_lga_batch_total_evals_dev(mdr_ctx* ctx, mdr_lga_batch* b, int64_t* d_total);
+/* Profiling replay (no graph): the same docking with CUDA events around the
+ * local-search kernels.  ls_ms = summed LS-kernel time (incl. polish),
+ * step_ms = whole step, ls_evals = evaluations done inside LS kernels. */
+int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds,
+                              float* ls_ms, float* step_ms, int64_t* ls_evals);
 
 #ifdef __cplusplus
 }

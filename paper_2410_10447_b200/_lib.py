@@ -55,12 +55,13 @@ _SIGS = {
     "mdr_lga_batch_run_dev": (I, [P, P, P]),
     "mdr_lga_batch_download": (I, [P, P, P, P, P, P, P, P, P]),
     "mdr_lga_batch_total_evals_dev": (I, [P, P, P]),
+    "mdr_lga_batch_profile_dev": (I, [P, P, P, P, P, P]),
 }
 
 # Optional entry points (present once their module is built).
 _OPTIONAL = {
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
-    "mdr_reduce_bench_kernels": (I, [P, I]),
+    "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
     "mdr_tc05_reduce4_dev": (I, [P, P, I, I, P]),
     "mdr_grid_build_dev": (I, []),

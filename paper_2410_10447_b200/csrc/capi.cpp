@@ -24,6 +24,19 @@
 
 using namespace mdr;
 
+struct mdr_dev_instance;
+struct mdr_lga_batch;
+
+// One cached docking setup for the host-buffer lga_run path: the device
+// ligand and the instantiated CUDA graph are reused while the shapes,
+// settings and method match (contents are re-uploaded every call).
+struct LgaCache {
+  int na = -1, ns = -1, nr = -1, method = -1, pair = -1, accum = -1, wpb = -1, R = -1;
+  mdr_lga_settings s{};
+  mdr_dev_instance* di = nullptr;
+  mdr_lga_batch* b = nullptr;
+};
+
 struct mdr_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -32,6 +45,7 @@ struct mdr_ctx {
   int wpb = 2;  // warps per CTA of the warp-per-pose kernels
   std::string err;
   uint64_t launches = 0;
+  LgaCache lga;
 };
 
 struct mdr_dev_instance {
@@ -169,6 +183,8 @@ mdr_ctx* mdr_ctx_create(int device) {
 void mdr_ctx_destroy(mdr_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
+  mdr_lga_batch_destroy(c, c->lga.b);
+  mdr_instance_free(c, c->lga.di);
   cudaStreamDestroy(c->own);
   delete c;
 }
@@ -346,6 +362,23 @@ int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int met
   return MDR_OK;
 }
 
+// C2 microbench: one block-level float4 reduce-and-broadcast per thread
+// block (see bench_reduce.cu for the kernel roster).
+int mdr_reduce_bench_kernels(void) { return kReduceBenchKernels; }
+const char* mdr_reduce_bench_kernel_name(int k) { return reduce_bench_name(k); }
+
+int mdr_reduce_bench_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in, int n_red, int chain_steps,
+                         float* d_out) {
+  if (!ctx || !d_in || !d_out || n_red <= 0 || kernel < 0 || kernel >= kReduceBenchKernels)
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (block < 64 || block > 1024 || block % 64)
+    return fail(ctx, MDR_ERR_BLOCK_SIZE, "bench blocks are multiples of 64 in [64, 1024]");
+  if (chain_steps > 0 && n_red % chain_steps) return fail(ctx, MDR_ERR_SIZE, "n_red must be a multiple of steps");
+  CK(launch_reduce_bench(kernel, block, d_in, n_red, chain_steps, d_out, 2048 / block, ctx->stream));
+  ctx->launches++;
+  return MDR_OK;
+}
+
 // ---------------------------------------------------------------- ligand
 static void torsion_axis_host(int k, double* out) {  // docking.cpp:181-189 (glibc, like the reference)
   constexpr double kGolden = 2.399963229728653;
@@ -372,9 +405,31 @@ static int check_instance(mdr_ctx* ctx, const mdr_instance* in) {
   return MDR_OK;
 }
 
-mdr_dev_instance* mdr_instance_upload(mdr_ctx* ctx, const mdr_instance* in) {
-  if (!ctx || check_instance(ctx, in) != MDR_OK) return nullptr;
+// Device layout of one ligand: a single allocation
+//   sites | atoms | torsion axes | torsion ids | fp32 sites | fp32 consts | box
+namespace {
+struct InstLayout {
+  size_t o_sites, o_atoms, o_tax, o_tors, o_sf, o_sf2, o_box, total;
+  explicit InstLayout(int na, int ns, int nr) {
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    o_sites = 0;
+    o_atoms = o_sites + al(sizeof(SiteD) * ns);
+    o_tax = o_atoms + al(sizeof(double4) * na);
+    o_tors = o_tax + al(sizeof(double) * 3 * (size_t)std::max(nr, 1));
+    o_sf = o_tors + al(sizeof(int) * na);
+    o_sf2 = o_sf + al(sizeof(float4) * ns);
+    o_box = o_sf2 + al(sizeof(float2) * ns);
+    total = o_box + al(sizeof(double) * 6);
+  }
+};
+
+// Host-side preparation + async copy of a ligand into an existing block of
+// the same shape.  The pair-loop constants and the random_genotype box are
+// computed here in the reference's evaluation order (docking.cpp:114-116,
+// 362-374); torsion axes with glibc like torsion_axis (docking.cpp:181-189).
+int write_instance(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_instance* in) {
   const int na = in->n_atoms, ns = in->n_sites, nr = in->n_rot;
+  const InstLayout lay(na, ns, nr);
   std::vector<SiteD> sites(ns);
   std::vector<float4> sf(ns);
   std::vector<float2> sf2(ns);
@@ -401,52 +456,55 @@ mdr_dev_instance* mdr_instance_upload(mdr_ctx* ctx, const mdr_instance* in) {
     }
     max_d0 = std::max(max_d0, d0);
   }
-  std::vector<double> taxes(3 * (size_t)std::max(nr, 1));
+  std::vector<double> taxes(3 * (size_t)std::max(nr, 1), 0.0);
   for (int k = 0; k < nr; ++k) torsion_axis_host(k, &taxes[3 * k]);
-  // one allocation: sites | atoms | taxes | tors | sites_f | sites_f2
-  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t o_sites = 0, b_sites = al(sizeof(SiteD) * ns);
-  const size_t o_atoms = o_sites + b_sites, b_atoms = al(sizeof(double4) * na);
-  const size_t o_tax = o_atoms + b_atoms, b_tax = al(sizeof(double) * taxes.size());
-  const size_t o_tors = o_tax + b_tax, b_tors = al(sizeof(int) * na);
-  const size_t o_sf = o_tors + b_tors, b_sf = al(sizeof(float4) * ns);
-  const size_t o_sf2 = o_sf + b_sf, b_sf2 = al(sizeof(float2) * ns);
-  const size_t total = o_sf2 + b_sf2;
+  const double margin = max_d0 + 1.0;  // random_genotype docking.cpp:374
+  double box[6];
+  for (int a = 0; a < 3; ++a) {
+    box[a] = lo[a] - margin;
+    box[3 + a] = hi[a] + margin;
+  }
+  char* b = static_cast<char*>(di->block);
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(b + lay.o_sites, sites.data(), sizeof(SiteD) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_atoms, in->atom_xyzw, sizeof(double) * 4 * na, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_tax, taxes.data(), sizeof(double) * taxes.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_tors, in->atom_torsion, sizeof(int) * na, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_sf, sf.data(), sizeof(float4) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_sf2, sf2.data(), sizeof(float2) * ns, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(b + lay.o_box, box, sizeof(box), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));  // host staging vectors die at return
+  return MDR_OK;
+}
+}  // namespace
+
+mdr_dev_instance* mdr_instance_upload(mdr_ctx* ctx, const mdr_instance* in) {
+  if (!ctx || check_instance(ctx, in) != MDR_OK) return nullptr;
+  const int na = in->n_atoms, ns = in->n_sites, nr = in->n_rot;
+  const InstLayout lay(na, ns, nr);
   mdr_dev_instance* di = new mdr_dev_instance;
-  if (cudaMalloc(&di->block, total) != cudaSuccess) {
+  if (cudaMalloc(&di->block, lay.total) != cudaSuccess) {
     fail(ctx, MDR_ERR_CUDA, "cudaMalloc failed for instance");
     delete di;
     return nullptr;
   }
-  char* b = static_cast<char*>(di->block);
-  cudaStream_t s = ctx->stream;
-  cudaMemcpyAsync(b + o_sites, sites.data(), sizeof(SiteD) * ns, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(b + o_atoms, in->atom_xyzw, sizeof(double) * 4 * na, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(b + o_tax, taxes.data(), sizeof(double) * taxes.size(), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(b + o_tors, in->atom_torsion, sizeof(int) * na, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(b + o_sf, sf.data(), sizeof(float4) * ns, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(b + o_sf2, sf2.data(), sizeof(float2) * ns, cudaMemcpyHostToDevice, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) {
-    fail(ctx, MDR_ERR_CUDA, "instance upload failed");
+  if (write_instance(ctx, di, in) != MDR_OK) {
     cudaFree(di->block);
     delete di;
     return nullptr;
   }
+  char* b = static_cast<char*>(di->block);
   LigandView& L = di->view;
   L.n_atoms = na;
   L.n_sites = ns;
   L.n_rot = nr;
-  L.sites = reinterpret_cast<const SiteD*>(b + o_sites);
-  L.atoms = reinterpret_cast<const double4*>(b + o_atoms);
-  L.taxes = reinterpret_cast<const double*>(b + o_tax);
-  L.tors = reinterpret_cast<const int*>(b + o_tors);
-  L.sites_f = reinterpret_cast<const float4*>(b + o_sf);
-  L.sites_f2 = reinterpret_cast<const float2*>(b + o_sf2);
-  const double margin = max_d0 + 1.0;  // random_genotype docking.cpp:374
-  for (int a = 0; a < 3; ++a) {
-    L.box_lo[a] = lo[a] - margin;
-    L.box_hi[a] = hi[a] + margin;
-  }
+  L.sites = reinterpret_cast<const SiteD*>(b + lay.o_sites);
+  L.atoms = reinterpret_cast<const double4*>(b + lay.o_atoms);
+  L.taxes = reinterpret_cast<const double*>(b + lay.o_tax);
+  L.tors = reinterpret_cast<const int*>(b + lay.o_tors);
+  L.sites_f = reinterpret_cast<const float4*>(b + lay.o_sf);
+  L.sites_f2 = reinterpret_cast<const float2*>(b + lay.o_sf2);
+  L.box = reinterpret_cast<const double*>(b + lay.o_box);
   di->n_atoms = na;
   di->n_sites = ns;
   di->n_rot = nr;
@@ -782,6 +840,40 @@ int mdr_lga_batch_run_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seed
   return MDR_OK;
 }
 
+int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds, float* ls_ms,
+                              float* step_ms, int64_t* ls_evals) {
+  if (!ctx || !b || !d_seeds) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  const LgaDev& D = b->D;
+  const int ne = 2 * D.gens + 4;
+  std::vector<cudaEvent_t> ev(ne);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaMemcpyAsync(b->seeds, d_seeds, sizeof(uint64_t) * D.R, cudaMemcpyDeviceToDevice, ctx->stream));
+  int launches = 0;
+  CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, &launches, ev.data()));
+  ctx->launches += (uint64_t)launches;
+  CK(cudaStreamSynchronize(ctx->stream));
+  float tot = 0.f, t = 0.f;
+  for (int g = 0; g <= D.gens; ++g) {
+    CK(cudaEventElapsedTime(&t, ev[2 * g], ev[2 * g + 1]));
+    tot += t;
+  }
+  CK(cudaEventElapsedTime(&t, ev[2 * D.gens + 2], ev[2 * D.gens + 3]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (ls_ms) *ls_ms = tot;
+  if (step_ms) *step_ms = t;
+  if (ls_evals) {
+    std::vector<mdr_ls_record> recs((size_t)D.R * D.maxrec);
+    std::vector<int> nrec(D.R);
+    CK(cudaMemcpy(recs.data(), D.recs, sizeof(mdr_ls_record) * recs.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(nrec.data(), D.nrec, sizeof(int) * D.R, cudaMemcpyDeviceToHost));
+    int64_t s = 0;
+    for (int r = 0; r < D.R; ++r)
+      for (int k = 0; k < std::min(nrec[r], D.maxrec); ++k) s += recs[(size_t)r * D.maxrec + k].iterations + 1;
+    *ls_evals = s;
+  }
+  return MDR_OK;
+}
+
 int mdr_lga_batch_total_evals_dev(mdr_ctx* ctx, mdr_lga_batch* b, int64_t* d_total) {
   if (!ctx || !b || !d_total) return fail(ctx, MDR_ERR_INVALID, "bad argument");
   CK(launch_lga_total(b->D, reinterpret_cast<long long*>(d_total), ctx->stream));
@@ -825,19 +917,35 @@ int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int ac
   if (int rc = check_instance(ctx, inst)) return rc;
   if (int rc = check_lga(ctx, method, s)) return rc;
   if (n_runs == 0) return MDR_OK;
-  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
-  if (!ig.di) return MDR_ERR_CUDA;
-  mdr_lga_batch* b = mdr_lga_batch_create(ctx, ig.di, method, accum, s, n_runs);
-  if (!b) return MDR_ERR_CUDA;
-  DevBuf<uint64_t> ds;
-  int rc = MDR_OK;
-  if (ds.alloc(n_runs, S(ctx)) != cudaSuccess ||
-      cudaMemcpyAsync(ds.p, seeds, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, S(ctx)) != cudaSuccess)
-    rc = fail(ctx, MDR_ERR_CUDA, "seed upload failed");
-  if (rc == MDR_OK) rc = mdr_lga_batch_run_dev(ctx, b, ds.p);
-  if (rc == MDR_OK) rc = mdr_lga_batch_download(ctx, b, best_e, best_g, evals, conv, n_records, records, total);
-  mdr_lga_batch_destroy(ctx, b);
-  return rc;
+  LgaCache& c = ctx->lga;
+  const bool hit = c.b && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
+                   c.method == method && c.pair == ctx->pair && c.accum == accum && c.wpb == ctx->wpb &&
+                   c.R == n_runs && std::memcmp(&c.s, s, sizeof *s) == 0;
+  if (hit) {
+    if (int rc = write_instance(ctx, c.di, inst)) return rc;
+  } else {
+    mdr_lga_batch_destroy(ctx, c.b);
+    mdr_instance_free(ctx, c.di);
+    c = LgaCache{};
+    c.di = mdr_instance_upload(ctx, inst);
+    if (!c.di) return MDR_ERR_CUDA;
+    c.b = mdr_lga_batch_create(ctx, c.di, method, accum, s, n_runs);
+    if (!c.b) return MDR_ERR_CUDA;
+    c.na = inst->n_atoms;
+    c.ns = inst->n_sites;
+    c.nr = inst->n_rot;
+    c.method = method;
+    c.pair = ctx->pair;
+    c.accum = accum;
+    c.wpb = ctx->wpb;
+    c.R = n_runs;
+    c.s = *s;
+  }
+  mdr_lga_batch* b = c.b;
+  CK(cudaMemcpyAsync(b->seeds, seeds, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaGraphLaunch(b->exec, S(ctx)));
+  ctx->launches += (uint64_t)b->launches;
+  return mdr_lga_batch_download(ctx, b, best_e, best_g, evals, conv, n_records, records, total);
 }
 
 }  // extern "C"

@@ -260,7 +260,7 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
     const uint64_t n = (uint64_t)p * D.dim + d + 1;
     double x;
     if (d < 3)
-      x = L.box_lo[d] + (L.box_hi[d] - L.box_lo[d]) * draw_unit(key, n);
+      x = L.box[d] + (L.box[3 + d] - L.box[d]) * draw_unit(key, n);
     else
       x = -kPi + (kPi - -kPi) * draw_unit(key, n);
     w.g[d] = x;
@@ -575,21 +575,29 @@ cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb) {
 // Enqueue a whole docking batch; prepare_lga() must have run (it is not
 // capture-safe, launch_lga is).
 cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
-                       int* n_launches) {
+                       int* n_launches, cudaEvent_t* ls_events) {
+  // ls_events (optional, profiling replay only): 2 per generation bracketing
+  // the LS kernel, then 2 bracketing the polish, then 2 bracketing the step.
   const size_t smem = warp_smem(L, wpb);
   int launches = 0;
+  if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 2], s);
   MDR_DISPATCH(method, pair, lga_init_kernel, <<<blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s>>>(L, D));
   lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
   launches += 2;
   for (int gen = 0; gen < D.gens; ++gen) {
     MDR_DISPATCH(method, pair, lga_offspring_kernel,
                  <<<blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s>>>(L, D, gen));
+    if (ls_events) cudaEventRecord(ls_events[2 * gen], s);
     if (D.L > 0)
       MDR_DISPATCH(method, pair, lga_ls_kernel, <<<blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s>>>(L, D));
+    if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
     lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
     launches += D.L > 0 ? 3 : 2;
   }
+  if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
   MDR_DISPATCH(method, pair, lga_polish_kernel, <<<blocks_for(D.R, wpb), 32 * wpb, smem, s>>>(L, D));
+  if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
+  if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;
   if (n_launches) *n_launches = launches;
   return cudaGetLastError();

@@ -20,7 +20,7 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
                                 int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb);
 cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb);
 cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
-                       int* n_launches);
+                       int* n_launches, cudaEvent_t* ls_events = nullptr);
 cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s);
 
 // reduce.cu
@@ -34,5 +34,11 @@ cudaError_t launch_reduce4(const float* vecs, int n, int n_red, int method, int 
                            cudaStream_t s);
 cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int half_mode, float* out,
                            cudaStream_t s);
+
+// bench_reduce.cu (C2 microbench)
+cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
+                                int blocks_per_sm, cudaStream_t s);
+const char* reduce_bench_name(int k);
+constexpr int kReduceBenchKernels = 5;
 
 }  // namespace mdr

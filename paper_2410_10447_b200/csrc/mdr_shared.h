@@ -33,7 +33,7 @@ struct LigandView {
   const double* taxes;      // torsion_axis(k) computed on the host (glibc)
   const float4* sites_f;    // fast-mode copy: x, y, z, depth
   const float2* sites_f2;   // fast-mode copy: c2, num
-  double box_lo[3], box_hi[3];  // random_genotype bounds incl. margin
+  const double* box;        // device: lo[3], hi[3] random_genotype bounds incl. margin
 };
 
 // All device state of a batch of LGA runs (docking.cpp:392-517).
