@@ -55,11 +55,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj]
         if src.endswith(".cu"):
-            cmd += ["-Xptxas", "-v"] if verbose else []
-        else:
-            cmd += ["-x", "cu"] if False else []
+            cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
+        else:  # host-only C++ (C-ABI, drop-in C++ API): g++, C++20, no FP contraction
+            cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
+                   f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include", "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for src, p in procs:
         out, _ = p.communicate()

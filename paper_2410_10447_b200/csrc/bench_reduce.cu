@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 
 #include "dock_launch.h"
+#include <cuda_bf16.h>
+
 #include "mdr_device.cuh"
 
 namespace mdr {
@@ -211,6 +213,99 @@ __device__ __forceinline__ float4 k2s(float4 v, Smem& sm, int it) {
   return block_exchange(acc[0] + acc[2], sm, it & 1, lane, warp, blockDim.x >> 5, false);
 }
 
+// ---------------------------------------------------------------- K1c
+// Two-level shuffle: warp transpose-reduce, then warp 0 folds the per-warp
+// partials with shuffles and publishes one float4 (2 syncs, few
+// instructions per thread).
+__device__ __forceinline__ float4 k1c(float4 v, Smem& sm, int it) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int buf = it & 1;
+  const float c = warp_transpose_reduce(v, lane);
+  if ((lane & 7) == 0) sm.part[buf][warp][lane >> 3] = c;
+  __syncthreads();
+  if (warp == 0) {
+    // lane l: component l & 3 of warps l>>2, (l>>2) + 8, ... (ascending)
+    float s = 0.f;
+    for (int w = lane >> 2; w < nw; w += 8) s += sm.part[buf][w][lane & 3];
+    s += __shfl_xor_sync(kFull, s, 4);
+    s += __shfl_xor_sync(kFull, s, 8);
+    s += __shfl_xor_sync(kFull, s, 16);
+    if (lane < 4) sm.result[buf][lane] = s;
+  }
+  __syncthreads();
+  return *reinterpret_cast<const float4*>(sm.result[buf]);
+}
+
+// ---------------------------------------------------------------- K2b
+// The paper's 2-sync tensor-core reduction made fp32-accurate: every value
+// is split into three bf16 terms (hi + mid + lo carry 24 significant bits,
+// bf16 keeps the fp32 exponent range so no scaling is needed), staged in the
+// paper's column-major packing, summed by m16n8k16 bf16 MMAs against P =
+// ones into fp32 accumulators; the Q fold (4 row groups) is 2 shuffles.
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+struct Bf16x3 {
+  uint32_t hi[2], mid[2], lo[2];  // (x,y), (z,e) pairs per term
+};
+__device__ __forceinline__ uint32_t bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
+  h = __bfloat162float(__float2bfloat16_rn(x));
+  const float r = x - h;  // exact
+  m = __bfloat162float(__float2bfloat16_rn(r));
+  l = r - m;  // exact; rounded to bf16 at packing
+}
+
+__device__ __forceinline__ float4 k2b(float4 v, Smem& sm, int it) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int B = blockDim.x;
+  __nv_bfloat16* t0 = reinterpret_cast<__nv_bfloat16*>(sm.tile);
+  float hx, mx, lx, hy, my, ly, hz, mz, lz, he, me, le;
+  split3(v.x, hx, mx, lx);
+  split3(v.y, hy, my, ly);
+  split3(v.z, hz, mz, lz);
+  split3(v.w, he, me, le);
+  uint2* s0 = reinterpret_cast<uint2*>(t0);
+  uint2* s1 = reinterpret_cast<uint2*>(t0 + 4 * B);
+  uint2* s2 = reinterpret_cast<uint2*>(t0 + 8 * B);
+  s0[threadIdx.x] = make_uint2(bf2(hx, hy), bf2(hz, he));
+  s1[threadIdx.x] = make_uint2(bf2(mx, my), bf2(mz, me));
+  s2[threadIdx.x] = make_uint2(bf2(lx, ly), bf2(lz, le));
+  __syncthreads();
+  const int buf = it & 1;
+  if (warp == 0) {
+    const int mat = lane >> 3, r = lane & 7;
+    const int col = r + 8 * (mat >> 1), rowoff = 8 * (mat & 1);
+    const uint32_t ones = 0x3F803F80u;  // bf16 1.0 pairs
+    float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f}, a2[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c = 0; c < B; c += 64) {
+      uint32_t f0[4], f1[4], f2[4];
+      ldsm_x4_trans(f0, reinterpret_cast<const __half*>(t0) + 4 * c + col * 16 + rowoff);
+      ldsm_x4_trans(f1, reinterpret_cast<const __half*>(t0 + 4 * B) + 4 * c + col * 16 + rowoff);
+      ldsm_x4_trans(f2, reinterpret_cast<const __half*>(t0 + 8 * B) + 4 * c + col * 16 + rowoff);
+      mma_bf16_16816(a0, f0, ones, ones);
+      mma_bf16_16816(a1, f1, ones, ones);
+      mma_bf16_16816(a2, f2, ones, ones);
+    }
+    // V rows g (d0) and g+8 (d2); W_c = V[c] + V[c+4] + V[c+8] + V[c+12]
+    const float r0 = (a0[0] + a1[0]) + a2[0], r2 = (a0[2] + a1[2]) + a2[2];
+    const float p = r0 + __shfl_down_sync(kFull, r0, 16);
+    const float q = r2 + __shfl_down_sync(kFull, r2, 16);
+    const int g = lane >> 2, t = lane & 3;
+    if (t == 0 && g < 4) sm.result[buf][g] = p + q;
+  }
+  __syncthreads();
+  return *reinterpret_cast<const float4*>(sm.result[buf]);
+}
+
 // ---------------------------------------------------------------- kernels
 template <int K>
 __device__ __forceinline__ float4 reduce_once(float4 v, Smem& sm, int it) {
@@ -218,7 +313,9 @@ __device__ __forceinline__ float4 reduce_once(float4 v, Smem& sm, int it) {
   if (K == 1) return k1b(v, sm, it);
   if (K == 2) return k2(v, sm, it);
   if (K == 3) return k2p(v, sm, it);
-  return k2s(v, sm, it);
+  if (K == 4) return k2s(v, sm, it);
+  if (K == 5) return k1c(v, sm, it);
+  return k2b(v, sm, it);
 }
 
 template <int K>
@@ -251,13 +348,16 @@ __global__ void stream_kernel(const float4* __restrict__ in, int n_red, float4* 
 }  // namespace bench
 
 static const char* kNames[] = {"reducefs_x4 (AutoDock, K1a)", "shuffle_transpose (K1b)", "wmma_f16 (paper, K2)",
-                               "split_tf32_block (K2p)", "split_tf32_warp (K2s)"};
+                               "split_tf32_block (K2p)", "split_tf32_warp (K2s)", "shuffle_2level (K1c)",
+                               "split_bf16x3_mma (K2b)"};
 
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
                                 int blocks_per_sm, cudaStream_t s) {
   const float4* i4 = reinterpret_cast<const float4*>(in);
   float4* o4 = reinterpret_cast<float4*>(out);
-  const size_t dyn = kernel == 2 ? (size_t)8 * block : (kernel >= 3 ? (size_t)16 * block : 0);
+  const size_t dyn = kernel == 2 ? (size_t)8 * block
+                     : kernel == 6 ? (size_t)24 * block
+                     : (kernel == 3 || kernel == 4) ? (size_t)16 * block : 0;
   if (chain_steps > 0) {
     const int grid = n_red / chain_steps;
 #define CH(K) bench::chain_kernel<K><<<grid, block, dyn, s>>>(i4, chain_steps, o4)
@@ -266,7 +366,9 @@ cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_re
       case 1: CH(1); break;
       case 2: CH(2); break;
       case 3: CH(3); break;
-      default: CH(4); break;
+      case 4: CH(4); break;
+      case 5: CH(5); break;
+      default: CH(6); break;
     }
 #undef CH
   } else {
@@ -278,13 +380,15 @@ cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_re
       case 1: ST(1); break;
       case 2: ST(2); break;
       case 3: ST(3); break;
-      default: ST(4); break;
+      case 4: ST(4); break;
+      case 5: ST(5); break;
+      default: ST(6); break;
     }
 #undef ST
   }
   return cudaGetLastError();
 }
 
-const char* reduce_bench_name(int k) { return (k >= 0 && k < 5) ? kNames[k] : "unknown"; }
+const char* reduce_bench_name(int k) { return (k >= 0 && k < kReduceBenchKernels) ? kNames[k] : "unknown"; }
 
 }  // namespace mdr

@@ -39,6 +39,6 @@ cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int 
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
                                 int blocks_per_sm, cudaStream_t s);
 const char* reduce_bench_name(int k);
-constexpr int kReduceBenchKernels = 5;
+constexpr int kReduceBenchKernels = 7;
 
 }  // namespace mdr

@@ -9,7 +9,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 # max |err| / sum|x| per kernel (K2 = the paper's f16 accumulator)
-TOL = {0: 1e-6, 1: 1e-6, 2: 2e-2, 3: 1e-6, 4: 1e-6}
+TOL = {0: 1e-6, 1: 1e-6, 2: 2e-2, 3: 1e-6, 4: 1e-6, 5: 1e-6, 6: 1e-6}
 
 
 @pytest.mark.parametrize("block", [64, 128, 256, 1024])
