@@ -45,6 +45,7 @@ from paper_2410_10447_b200._abi import (  # noqa: E402
     HALF,
     PAIR_FP32,
     PAIR_FP64,
+    PAIR_FP64_FAST,
     SINGLE,
     TCU,
     TCU_SPLIT,
@@ -268,7 +269,7 @@ def run_gpu_arm(args):
     from paper_2410_10447_b200._lib import load
 
     lib = load()
-    pair = PAIR_FP32 if args.pair == "fp32" else PAIR_FP64
+    pair = {"fp64": PAIR_FP64, "fp32": PAIR_FP32, "fp64fast": PAIR_FP64_FAST}[args.pair]
     dev = Device(local, pair=pair, warps_per_block=args.wpb)
     # a dedicated (non-default) stream shared by torch and the library, so the
     # CUDA events below bracket exactly the library's work
@@ -437,7 +438,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--method", default="baseline", choices=list(METHODS))
-    ap.add_argument("--pair", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--pair", default="fp64", choices=["fp64", "fp64fast", "fp32"])
     ap.add_argument("--wpb", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -49,8 +49,9 @@ enum { MDR_ACCUM_HALF = 0, MDR_ACCUM_SINGLE = 1 };
 enum { MDR_LAYOUT_ROW = 0, MDR_LAYOUT_COL = 1 };
 /* pair-term arithmetic of the scoring kernel: FP64 reproduces the
  * reference's double evaluate_atoms (docking.cpp:95-128) bit for bit;
- * FP32 is the fast mode (tolerance parity only). */
-enum { MDR_PAIR_FP64 = 0, MDR_PAIR_FP32 = 1 };
+ * FP64_FAST (FMA, one reciprocal per pair, sites split across the warps of
+ * a CTA) and FP32 are the fast modes (tolerance parity). */
+enum { MDR_PAIR_FP64 = 0, MDR_PAIR_FP32 = 1, MDR_PAIR_FP64_FAST = 2 };
 
 /* ---- plain-data structs ------------------------------------------------ */
 /* SyncStats reduce.hpp:33-54 (field order preserved). */
@@ -106,6 +107,9 @@ void* mdr_ctx_stream(mdr_ctx* ctx);
 int mdr_ctx_set_pair_precision(mdr_ctx* ctx, int pair_precision);
 /* Warps per CTA of the warp-per-pose kernels (1..16, default 2). */
 int mdr_ctx_set_warps_per_block(mdr_ctx* ctx, int warps);
+/* Warps cooperating on one pose in the CTA-per-pose local-search kernels
+ * used by the fast pair modes (1..16, default 4). */
+int mdr_ctx_set_cta_warps(mdr_ctx* ctx, int warps);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);
 /* Number of kernel launches this context has enqueued so far. */
@@ -142,6 +146,10 @@ int mdr_warp_reduce_batch(mdr_ctx* ctx, const float* lanes, int n_red,
 /* reduce7 reduce.cpp:165-209.  recs: n_red x n x {e,gx,gy,gz,tx,ty,tz}. */
 int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red,
                       int method, int accum, float* out, mdr_sync_stats* stats);
+
+/* Self test: bit mismatches of the branch-free FP64 division of the strict
+ * pair loop against IEEE div.rn.f64 over n counter-generated operand pairs. */
+int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
 
 /* C2 microbench (no reference counterpart; cli.cpp:195-266 is its CPU
  * analogue): kernel k in [0, mdr_reduce_bench_kernels()) reduces float4 per

@@ -9,6 +9,7 @@ from ._abi import (  # noqa: F401
     HALF,
     PAIR_FP32,
     PAIR_FP64,
+    PAIR_FP64_FAST,
     SINGLE,
     TCU,
     TCU_SPLIT,

@@ -19,7 +19,7 @@ import numpy as np
 OK, ERR_SIZE, ERR_BLOCK_SIZE, ERR_NUMERIC_DOMAIN, ERR_PARSE, ERR_CUDA, ERR_INVALID = range(7)
 BASELINE, TCU, TCU_SPLIT = 0, 1, 2
 HALF, SINGLE = 0, 1
-PAIR_FP64, PAIR_FP32 = 0, 1
+PAIR_FP64, PAIR_FP32, PAIR_FP64_FAST = 0, 1, 2
 
 
 class SizeError(ValueError):

@@ -29,6 +29,7 @@ _SIGS = {
     "mdr_ctx_stream": (P, [P]),
     "mdr_ctx_set_pair_precision": (I, [P, I]),
     "mdr_ctx_set_warps_per_block": (I, [P, I]),
+    "mdr_ctx_set_cta_warps": (I, [P, I]),
     "mdr_last_error": (C.c_char_p, [P]),
     "mdr_ctx_launch_count": (U64, [P]),
     "mdr_ctx_synchronize": (I, [P]),
@@ -56,6 +57,10 @@ _SIGS = {
     "mdr_lga_batch_download": (I, [P, P, P, P, P, P, P, P, P]),
     "mdr_lga_batch_total_evals_dev": (I, [P, P, P]),
     "mdr_lga_batch_profile_dev": (I, [P, P, P, P, P, P]),
+    "mdr_selftest_ddiv": (I, [P, U64, C.c_int64, P]),
+    "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
+    "mdr_reduce_bench_kernels": (I, []),
+    "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
 }
 
 # Optional entry points (present once their module is built).

@@ -42,7 +42,8 @@ struct mdr_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   int pair = MDR_PAIR_FP64;
-  int wpb = 2;  // warps per CTA of the warp-per-pose kernels
+  int wpb = 2;        // warps per CTA of the warp-per-pose kernels
+  int cta_warps = 4;  // warps per pose of the CTA-per-pose kernels (fast pair modes)
   std::string err;
   uint64_t launches = 0;
   LgaCache lga;
@@ -162,6 +163,11 @@ struct DevBuf {
 
 cudaStream_t S(mdr_ctx* c) { return c->stream; }
 
+// The CTA-per-pose local search is used for the fast pair modes; the
+// bit-faithful FP64 mode keeps the warp-per-pose kernels (sites summed in
+// the reference's order).
+int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 ? 0 : c->cta_warps; }
+
 }  // namespace
 
 extern "C" {
@@ -197,8 +203,14 @@ int mdr_ctx_set_stream(mdr_ctx* c, void* s) {
 void* mdr_ctx_stream(mdr_ctx* c) { return c ? c->stream : nullptr; }
 
 int mdr_ctx_set_pair_precision(mdr_ctx* c, int p) {
-  if (!c || (p != MDR_PAIR_FP64 && p != MDR_PAIR_FP32)) return fail(c, MDR_ERR_INVALID, "bad pair precision");
+  if (!c || p < MDR_PAIR_FP64 || p > MDR_PAIR_FP64_FAST) return fail(c, MDR_ERR_INVALID, "bad pair precision");
   c->pair = p;
+  return MDR_OK;
+}
+
+int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
+  if (!c || w < 1 || w > 16) return fail(c, MDR_ERR_INVALID, "CTA warps must be 1..16");
+  c->cta_warps = w;
   return MDR_OK;
 }
 
@@ -359,6 +371,22 @@ int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int met
   ctx->launches++;
   CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 28, cudaMemcpyDeviceToHost, S(ctx)));
   CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+// Self test of the branch-free FP64 division used by the strict pair loop:
+// number of bit mismatches against IEEE div.rn.f64 over n operand pairs.
+int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches) {
+  if (!ctx || !mismatches || n < 0) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  DevBuf<unsigned long long> d;
+  CK(d.alloc(1, S(ctx)));
+  CK(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), S(ctx)));
+  CK(launch_ddiv_selftest(seed, (long long)n, d.p, S(ctx)));
+  ctx->launches++;
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  *mismatches = h;
   return MDR_OK;
 }
 
@@ -628,7 +656,7 @@ int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double*
   if (int rc = check_partition(ctx, partition, method)) return rc;
   if (n <= 0) return MDR_OK;
   CK(launch_local_search(di->view, starts, n, max_iters, tol, method, ctx->pair, partition, accum == MDR_ACCUM_HALF,
-                         og, oe, oit, ocv, status, ctx->stream, ctx->wpb));
+                         og, oe, oit, ocv, status, ctx->stream, ctx->wpb, cta_warps_for(ctx)));
   ctx->launches++;
   return MDR_OK;
 }
@@ -705,6 +733,7 @@ struct mdr_lga_batch {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t captured_on = nullptr;
   int launches = 0;
+  int cta_warps = 0;
   mdr_lga_settings settings{};
 };
 
@@ -804,9 +833,10 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
     delete b;
     return nullptr;
   }
-  cudaError_t e = prepare_lga(b->L, method, b->pair, ctx->wpb);
+  b->cta_warps = cta_warps_for(ctx);
+  cudaError_t e = prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-  if (e == cudaSuccess) e = launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, &b->launches);
+  if (e == cudaSuccess) e = launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, b->cta_warps, &b->launches);
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(cs, &g);
   if (e == cudaSuccess) e = e2;
@@ -849,7 +879,7 @@ int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaMemcpyAsync(b->seeds, d_seeds, sizeof(uint64_t) * D.R, cudaMemcpyDeviceToDevice, ctx->stream));
   int launches = 0;
-  CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, &launches, ev.data()));
+  CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, b->cta_warps, &launches, ev.data()));
   ctx->launches += (uint64_t)launches;
   CK(cudaStreamSynchronize(ctx->stream));
   float tot = 0.f, t = 0.f;
@@ -918,7 +948,7 @@ int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int ac
   if (int rc = check_lga(ctx, method, s)) return rc;
   if (n_runs == 0) return MDR_OK;
   LgaCache& c = ctx->lga;
-  const bool hit = c.b && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
+  const bool hit = c.b && c.b->cta_warps == cta_warps_for(ctx) && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
                    c.method == method && c.pair == ctx->pair && c.accum == accum && c.wpb == ctx->wpb &&
                    c.R == n_runs && std::memcmp(&c.s, s, sizeof *s) == 0;
   if (hit) {

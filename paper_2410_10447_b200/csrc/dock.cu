@@ -80,7 +80,7 @@ __global__ void scoreref_kernel(LigandView L, const double* __restrict__ genos, 
   double e = 0.0;
   d3 gs = {0, 0, 0}, ts = {0, 0, 0};
   for (int i = lane; i < S.n_atoms; i += 32) {
-    const Partial p = atom_partial_fp64(S, g, f.R, tr, i);
+    const Partial p = atom_partial<MDR_PAIR_FP64>(S, g, f.R, tr, i);
     e += p.e;
     gs = gs + p.g;
     ts = ts + p.t;
@@ -92,7 +92,7 @@ __global__ void scoreref_kernel(LigandView L, const double* __restrict__ genos, 
   for (int k = 0; k < S.n_rot; ++k) {
     d3 tk = {0, 0, 0};
     for (int i = lane; i < S.n_atoms; i += 32)
-      if (S.tors[i] == k) tk = tk + atom_partial_fp64(S, g, f.R, tr, i).t;
+      if (S.tors[i] == k) tk = tk + atom_partial<MDR_PAIR_FP64>(S, g, f.R, tr, i).t;
     tk = {warp_sum_d(tk.x), warp_sum_d(tk.y), warp_sum_d(tk.z)};
     if (lane == 0) {
       const d3 ax = mv(f.R, d3{S.taxes[3 * k], S.taxes[3 * k + 1], S.taxes[3 * k + 2]});
@@ -239,6 +239,156 @@ __global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n
   }
 }
 
+// ------------------------------------------ K4c local search, CTA per pose
+// Fast pair modes only: the W warps of a CTA split the receptor sites of
+// every evaluation (warp w sums sites [w*S/W, (w+1)*S/W) for all atoms, one
+// atom per lane), warp 0 merges the per-warp partials, runs the slot
+// reduction and the ADADELTA step; two CTA barriers per evaluation.
+struct CtaCtx {
+  WarpScratch ws;  // warp 0's reduction scratch
+  double* g;       // [kMaxDim] current genotype
+  double* best;    // [kMaxDim] best genotype
+  double* part;    // [W][n_atoms][4] per-warp partial (e, gx, gy, gz)
+  int* ctl;        // [0]: stop flag
+};
+
+__host__ __device__ inline size_t cta_region_bytes(int n_atoms, int warps) {
+  return (size_t)kWarpScratchBytes + 2 * kMaxDim * 8 + (size_t)warps * n_atoms * 32 + 16;
+}
+
+__device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, int warps) {
+  CtaCtx c;
+  c.ws.tile = reinterpret_cast<__half*>(base);
+  c.ws.rec = reinterpret_cast<float*>(base + 2 * 256 * 2);
+  c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
+  c.best = c.g + kMaxDim;
+  c.part = c.best + kMaxDim;
+  c.ctl = reinterpret_cast<int*>(c.part + (size_t)warps * n_atoms * 4);
+  return c;
+}
+
+// local_search docking.cpp:310-351 by the whole CTA; the result is valid in
+// warp 0, the best genotype in c.best.
+template <int METHOD, int PAIR>
+__device__ LsResult local_search_cta(const SmemLigand& S, const double* start, int max_iters, double tol,
+                                     int partition, bool half_mode, const CtaCtx& c) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+  const int dim = 6 + S.n_rot;
+  const double rho = 0.95, eps = 1e-6;
+  for (int d = threadIdx.x; d < dim; d += blockDim.x) {
+    const double x = d >= 3 ? wrap_angle(start[d]) : start[d];
+    c.g[d] = x;
+    c.best[d] = x;
+  }
+  __syncthreads();
+  const int j0 = warp * S.n_sites / W, j1 = (warp + 1) * S.n_sites / W;
+  double sg0 = 0.0, su0 = 0.0, sg1 = 0.0, su1 = 0.0, hist = 0.0;
+  LsResult r;
+  r.energy = 0.0;
+  r.iterations = 0;
+  r.converged = 0;
+  r.status = MDR_OK;
+  for (int iter = 0;; ++iter) {
+    const Frame f = build_frame(c.g[3], c.g[4], c.g[5]);
+    const d3 tr = {c.g[0], c.g[1], c.g[2]};
+    for (int i = lane; i < S.n_atoms; i += 32) {
+      const d3 world = atom_world(S, c.g, f.R, tr, i);
+      double e = 0.0;
+      d3 gg = {0.0, 0.0, 0.0};
+      pair_range<PAIR>(S, world, S.atoms[i].w, j0, j1, e, gg);
+      double* q = c.part + ((size_t)warp * S.n_atoms + i) * 4;
+      q[0] = e;
+      q[1] = gg.x;
+      q[2] = gg.y;
+      q[3] = gg.z;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const ScoreOut o = reduce_atoms<METHOD>(S.n_atoms, partition, half_mode, c.ws, [&](int i) {
+        Partial p;
+        p.e = 0.0;
+        p.g = {0.0, 0.0, 0.0};
+        for (int w = 0; w < W; ++w) {
+          const double* q = c.part + ((size_t)w * S.n_atoms + i) * 4;
+          p.e += q[0];
+          p.g = p.g + d3{q[1], q[2], q[3]};
+        }
+        p.t = cross(atom_world(S, c.g, f.R, tr, i) - tr, p.g);
+        return p;
+      });
+      const float gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
+      const float gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+      const double e = (double)o.sums[0];
+      bool done = false;
+      if (iter == 0) {
+        r.energy = e;
+        hist = e;
+      } else {
+        if (e < r.energy) {
+          r.energy = e;
+          for (int d = lane; d < dim; d += 32) c.best[d] = c.g[d];
+        }
+        const int slot = iter & (kWindow - 1);
+        const double old = __shfl_sync(kFull, hist, slot);
+        if (lane == slot) hist = r.energy;
+        r.iterations = iter;
+        if (iter >= kWindow && old - r.energy < tol) {
+          r.converged = 1;
+          done = true;
+        }
+      }
+      if (!done && iter >= max_iters) done = true;
+      if (!done) {
+        const bool bad = (lane < dim && !isfinite(gr0)) || (lane + 32 < dim && !isfinite(gr1));
+        if (__any_sync(kFull, bad)) {
+          r.status = MDR_ERR_NUMERIC_DOMAIN;
+          done = true;
+        } else {
+          if (lane < dim) {
+            double x = c.g[lane];
+            adadelta_dim(sg0, su0, x, (double)gr0, lane, rho, eps);
+            c.g[lane] = x;
+          }
+          if (lane + 32 < dim) {
+            double x = c.g[lane + 32];
+            adadelta_dim(sg1, su1, x, (double)gr1, lane + 32, rho, eps);
+            c.g[lane + 32] = x;
+          }
+        }
+      }
+      if (lane == 0) c.ctl[0] = done;
+    }
+    __syncthreads();
+    if (c.ctl[0]) break;
+    __syncthreads();  // ctl is rewritten by warp 0 next evaluation
+  }
+  return r;
+}
+
+template <int METHOD, int PAIR>
+__global__ void ls_cta_kernel(LigandView L, const double* __restrict__ starts, int n, int max_iters, double tol,
+                              int partition, int half_mode, double* __restrict__ out_g, double* __restrict__ out_e,
+                              int* __restrict__ out_it, int* __restrict__ out_cv, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int item = blockIdx.x;
+  if (item >= n) return;
+  const CtaCtx c = cta_region(smem + ligand_smem_bytes(L), L.n_atoms, blockDim.x >> 5);
+  const int dim = 6 + L.n_rot;
+  const LsResult r = local_search_cta<METHOD, PAIR>(S, starts + (size_t)item * dim, max_iters, tol, partition,
+                                                    half_mode != 0, c);
+  if (threadIdx.x < 32) {
+    for (int d = threadIdx.x; d < dim; d += 32) out_g[(size_t)item * dim + d] = c.best[d];
+    if (threadIdx.x == 0) {
+      out_e[item] = r.energy;
+      out_it[item] = r.iterations;
+      out_cv[item] = r.converged;
+      if (r.status != MDR_OK) status[item] = r.status;
+    }
+  }
+}
+
 // ------------------------------------------------------------- K5 LGA
 __device__ __forceinline__ uint64_t run_key(const LgaDev& D, int run) {
   return mix64(D.seeds[run] ^ D.label_hash);  // RngStream ctor rng.cpp:31-32
@@ -352,6 +502,55 @@ __global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
   if (lane == 0) ne[1 + i] = (double)o.sums[0];
 }
 
+// Index (1..off) of the offspring of rank r in the stable (energy, index)
+// order of docking.cpp:476-483; every lane of the calling warp gets it.
+__device__ __forceinline__ int ls_target(const LgaDev& D, int run, int r) {
+  const int lane = threadIdx.x & 31;
+  const double* ne = D.pope[D.cur[run] ^ 1] + (size_t)run * D.P;
+  int target = -1;
+  for (int j = 1 + lane; j <= D.off; j += 32) {
+    const double ej = ne[j];
+    int rank = 0;
+    for (int k = 1; k <= D.off; ++k) {
+      const double ek = ne[k];
+      rank += (ek < ej) || (ek == ej && k < j);
+    }
+    if (rank == r) target = j;
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) target = max(target, __shfl_xor_sync(kFull, target, off));
+  return target;
+}
+
+// Fast pair modes: one CTA per local search (CTA-per-pose kernel K4c).
+template <int METHOD, int PAIR>
+__global__ void lga_ls_cta_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int item = blockIdx.x;
+  if (item >= D.R * D.L) return;
+  const int run = item / D.L, r = item % D.L;
+  if (!D.active[run]) return;
+  const CtaCtx cc = cta_region(smem + ligand_smem_bytes(L), L.n_atoms, blockDim.x >> 5);
+  const int c = D.cur[run];
+  const int target = ls_target(D, run, r);
+  const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
+  const LsResult res = local_search_cta<METHOD, PAIR>(S, start, D.ls_iters, D.tol, D.partition, D.half_mode != 0,
+                                                      cc);
+  if (threadIdx.x < 32) {
+    const size_t o = (size_t)run * D.L + r;
+    for (int d = threadIdx.x; d < D.dim; d += 32) D.lsg[o * D.dim + d] = cc.best[d];
+    if (threadIdx.x == 0) {
+      D.lse[o] = res.energy;
+      D.lsit[o] = res.iterations;
+      D.lscv[o] = res.converged;
+      D.lstarget[o] = target;
+      if (res.status != MDR_OK) D.status[run] = res.status;
+    }
+  }
+}
+
 // Lamarckian step: the r-th best offspring (stable by index) refined by a
 // device-resident local search (docking.cpp:476-489).
 template <int METHOD, int PAIR>
@@ -366,20 +565,7 @@ __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
   if (!D.active[run]) return;
   WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
   const int c = D.cur[run];
-  const double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
-  // rank of offspring j (1..off) by (energy, index); pick rank r
-  int target = -1;
-  for (int j = 1 + lane; j <= D.off; j += 32) {
-    const double ej = ne[j];
-    int rank = 0;
-    for (int k = 1; k <= D.off; ++k) {
-      const double ek = ne[k];
-      rank += (ek < ej) || (ek == ej && k < j);
-    }
-    if (rank == r) target = j;
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) target = max(target, __shfl_xor_sync(kFull, target, off));
+  const int target = ls_target(D, run, r);
   const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
   const LsResult res = local_search_warp<METHOD, PAIR>(S, start, D.ls_iters, D.tol, D.partition,
                                                        D.half_mode != 0, w);
@@ -461,6 +647,35 @@ __global__ void lga_polish_kernel(LigandView L, LgaDev D) {
   }
 }
 
+template <int METHOD, int PAIR>
+__global__ void lga_polish_cta_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int run = blockIdx.x;
+  if (run >= D.R || D.status[run] != MDR_OK) return;
+  const long long remaining = D.max_evals - D.evals[run];
+  if (remaining <= 1) {
+    if (threadIdx.x == 0) D.conv[run] = 0;
+    return;
+  }
+  const int iters = (int)((long long)D.ls_iters < remaining - 1 ? (long long)D.ls_iters : remaining - 1);
+  const CtaCtx cc = cta_region(smem + ligand_smem_bytes(L), L.n_atoms, blockDim.x >> 5);
+  const LsResult res = local_search_cta<METHOD, PAIR>(S, D.best_g + (size_t)run * D.dim, iters, D.tol, D.partition,
+                                                      D.half_mode != 0, cc);
+  __syncthreads();  // every warp has finished reading best_g before it is updated
+  if (threadIdx.x == 0) {
+    if (res.status != MDR_OK) {
+      D.status[run] = res.status;
+      return;
+    }
+    D.evals[run] += res.iterations + 1;
+    track_best(D, run, cc.best, res.energy);
+    push_record(D, run, res.energy, res.iterations, res.converged);
+    D.conv[run] = res.converged;
+  }
+}
+
 __global__ void lga_total_evals(LgaDev D, long long* out) {
   long long s = 0;
   for (int r = threadIdx.x; r < D.R; r += blockDim.x) s += D.evals[r];
@@ -485,49 +700,57 @@ static cudaError_t prep(K kernel, size_t smem) {
   return cudaSuccess;
 }
 
-#define MDR_DISPATCH(METHOD_VAR, PAIR_VAR, KERNEL, ...)                                        \
-  do {                                                                                         \
-    if (METHOD_VAR == MDR_METHOD_BASELINE && PAIR_VAR == MDR_PAIR_FP64)                        \
-      KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64> __VA_ARGS__;                                  \
-    else if (METHOD_VAR == MDR_METHOD_TCU && PAIR_VAR == MDR_PAIR_FP64)                        \
-      KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64> __VA_ARGS__;                                       \
-    else if (METHOD_VAR == MDR_METHOD_TCU_SPLIT && PAIR_VAR == MDR_PAIR_FP64)                  \
-      KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64> __VA_ARGS__;                                 \
-    else if (METHOD_VAR == MDR_METHOD_BASELINE)                                                \
-      KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32> __VA_ARGS__;                                  \
-    else if (METHOD_VAR == MDR_METHOD_TCU)                                                     \
-      KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32> __VA_ARGS__;                                       \
-    else                                                                                       \
-      KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32> __VA_ARGS__;                                 \
-  } while (0)
+#define MDR_GEN_DISPATCH(KERNEL)                                                                     \
+  template <class... A>                                                                              \
+  static void dispatch_##KERNEL(int method, int pair, dim3 g, dim3 b, size_t smem, cudaStream_t s,   \
+                                A... args) {                                                         \
+    switch (method * 3 + pair) {                                                                     \
+      case 0: KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;         \
+      case 1: KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;         \
+      case 2: KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;    \
+      case 3: KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;              \
+      case 4: KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;              \
+      case 5: KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;         \
+      case 6: KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;        \
+      case 7: KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;        \
+      default: KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;  \
+    }                                                                                                \
+  }                                                                                                  \
+  static cudaError_t prep_##KERNEL(int method, int pair, size_t smem) {                              \
+    switch (method * 3 + pair) {                                                                     \
+      case 0: return prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64>, smem);                         \
+      case 1: return prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32>, smem);                         \
+      case 2: return prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64_FAST>, smem);                    \
+      case 3: return prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64>, smem);                              \
+      case 4: return prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32>, smem);                              \
+      case 5: return prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64_FAST>, smem);                         \
+      case 6: return prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64>, smem);                        \
+      case 7: return prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32>, smem);                        \
+      default: return prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64_FAST>, smem);                  \
+    }                                                                                                \
+  }
 
-#define MDR_PREP(METHOD_VAR, PAIR_VAR, KERNEL, SMEM, ERR)                                      \
-  do {                                                                                         \
-    if (METHOD_VAR == MDR_METHOD_BASELINE && PAIR_VAR == MDR_PAIR_FP64)                        \
-      ERR = prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP64>, SMEM);                            \
-    else if (METHOD_VAR == MDR_METHOD_TCU && PAIR_VAR == MDR_PAIR_FP64)                        \
-      ERR = prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP64>, SMEM);                                 \
-    else if (METHOD_VAR == MDR_METHOD_TCU_SPLIT && PAIR_VAR == MDR_PAIR_FP64)                  \
-      ERR = prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64>, SMEM);                           \
-    else if (METHOD_VAR == MDR_METHOD_BASELINE)                                                \
-      ERR = prep(KERNEL<MDR_METHOD_BASELINE, MDR_PAIR_FP32>, SMEM);                            \
-    else if (METHOD_VAR == MDR_METHOD_TCU)                                                     \
-      ERR = prep(KERNEL<MDR_METHOD_TCU, MDR_PAIR_FP32>, SMEM);                                 \
-    else                                                                                       \
-      ERR = prep(KERNEL<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32>, SMEM);                           \
-  } while (0)
+MDR_GEN_DISPATCH(score_kernel)
+MDR_GEN_DISPATCH(ls_kernel)
+MDR_GEN_DISPATCH(ls_cta_kernel)
+MDR_GEN_DISPATCH(lga_init_kernel)
+MDR_GEN_DISPATCH(lga_offspring_kernel)
+MDR_GEN_DISPATCH(lga_ls_kernel)
+MDR_GEN_DISPATCH(lga_ls_cta_kernel)
+MDR_GEN_DISPATCH(lga_polish_kernel)
+MDR_GEN_DISPATCH(lga_polish_cta_kernel)
 
 static inline int blocks_for(long long items, int wpb) { return (int)((items + wpb - 1) / wpb); }
+static size_t cta_smem(const LigandView& L, int cw) { return ligand_smem_bytes(L) + cta_region_bytes(L.n_atoms, cw); }
 
 cudaError_t launch_score(const LigandView& L, const double* genos, int n, int method, int pair, int partition,
                          int half_mode, float* energy, float* grad, float* torque, cudaStream_t s, int wpb) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = warp_smem(L, wpb);
-  cudaError_t e = cudaSuccess;
-  MDR_PREP(method, pair, score_kernel, smem, e);
+  cudaError_t e = prep_score_kernel(method, pair, smem);
   if (e != cudaSuccess) return e;
-  MDR_DISPATCH(method, pair, score_kernel,
-               <<<blocks_for(n, wpb), 32 * wpb, smem, s>>>(L, genos, n, partition, half_mode, energy, grad, torque));
+  dispatch_score_kernel(method, pair, blocks_for(n, wpb), 32 * wpb, smem, s, L, genos, n, partition, half_mode,
+                        energy, grad, torque);
   return cudaGetLastError();
 }
 
@@ -550,52 +773,73 @@ cudaError_t launch_adadelta(int dim, int n, double rho, double eps, double* sq_g
 
 cudaError_t launch_local_search(const LigandView& L, const double* starts, int n, int max_iters, double tol,
                                 int method, int pair, int partition, int half_mode, double* out_g, double* out_e,
-                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb) {
+                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb, int cta_warps) {
   if (n <= 0) return cudaSuccess;
-  const size_t smem = warp_smem(L, wpb);
-  cudaError_t e = cudaSuccess;
-  MDR_PREP(method, pair, ls_kernel, smem, e);
-  if (e != cudaSuccess) return e;
-  MDR_DISPATCH(method, pair, ls_kernel,
-               <<<blocks_for(n, wpb), 32 * wpb, smem, s>>>(L, starts, n, max_iters, tol, partition, half_mode,
-                                                           out_g, out_e, out_it, out_cv, status));
+  cudaError_t e;
+  if (cta_warps > 0) {
+    const size_t smem = cta_smem(L, cta_warps);
+    e = prep_ls_cta_kernel(method, pair, smem);
+    if (e != cudaSuccess) return e;
+    dispatch_ls_cta_kernel(method, pair, n, 32 * cta_warps, smem, s, L, starts, n, max_iters, tol, partition,
+                           half_mode, out_g, out_e, out_it, out_cv, status);
+  } else {
+    const size_t smem = warp_smem(L, wpb);
+    e = prep_ls_kernel(method, pair, smem);
+    if (e != cudaSuccess) return e;
+    dispatch_ls_kernel(method, pair, blocks_for(n, wpb), 32 * wpb, smem, s, L, starts, n, max_iters, tol, partition,
+                       half_mode, out_g, out_e, out_it, out_cv, status);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb) {
+cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps) {
   const size_t smem = warp_smem(L, wpb);
-  cudaError_t e = cudaSuccess;
-  MDR_PREP(method, pair, lga_init_kernel, smem, e);
-  if (e == cudaSuccess) MDR_PREP(method, pair, lga_offspring_kernel, smem, e);
-  if (e == cudaSuccess) MDR_PREP(method, pair, lga_ls_kernel, smem, e);
-  if (e == cudaSuccess) MDR_PREP(method, pair, lga_polish_kernel, smem, e);
+  cudaError_t e = prep_lga_init_kernel(method, pair, smem);
+  if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, smem);
+  if (cta_warps > 0) {
+    const size_t cs = cta_smem(L, cta_warps);
+    if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cs);
+    if (e == cudaSuccess) e = prep_lga_polish_cta_kernel(method, pair, cs);
+  } else {
+    if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, smem);
+    if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, smem);
+  }
   return e;
 }
 
 // Enqueue a whole docking batch; prepare_lga() must have run (it is not
-// capture-safe, launch_lga is).
+// capture-safe, launch_lga is).  cta_warps > 0 selects the CTA-per-pose
+// local-search kernels.
 cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
-                       int* n_launches, cudaEvent_t* ls_events) {
+                       int cta_warps, int* n_launches, cudaEvent_t* ls_events) {
   // ls_events (optional, profiling replay only): 2 per generation bracketing
   // the LS kernel, then 2 bracketing the polish, then 2 bracketing the step.
   const size_t smem = warp_smem(L, wpb);
+  const size_t cs = cta_smem(L, cta_warps > 0 ? cta_warps : 1);
   int launches = 0;
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 2], s);
-  MDR_DISPATCH(method, pair, lga_init_kernel, <<<blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s>>>(L, D));
+  dispatch_lga_init_kernel(method, pair, blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s, L, D);
   lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
   launches += 2;
   for (int gen = 0; gen < D.gens; ++gen) {
-    MDR_DISPATCH(method, pair, lga_offspring_kernel,
-                 <<<blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s>>>(L, D, gen));
+    dispatch_lga_offspring_kernel(method, pair, blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s, L, D,
+                                  gen);
     if (ls_events) cudaEventRecord(ls_events[2 * gen], s);
-    if (D.L > 0)
-      MDR_DISPATCH(method, pair, lga_ls_kernel, <<<blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s>>>(L, D));
+    if (D.L > 0) {
+      if (cta_warps > 0)
+        dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
+      else
+        dispatch_lga_ls_kernel(method, pair, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
+    }
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
     lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
     launches += D.L > 0 ? 3 : 2;
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
-  MDR_DISPATCH(method, pair, lga_polish_kernel, <<<blocks_for(D.R, wpb), 32 * wpb, smem, s>>>(L, D));
+  if (cta_warps > 0)
+    dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * cta_warps, cs, s, L, D);
+  else
+    dispatch_lga_polish_kernel(method, pair, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;

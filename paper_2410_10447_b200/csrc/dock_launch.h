@@ -17,10 +17,10 @@ cudaError_t launch_adadelta(int dim, int n, double rho, double eps, double* sq_g
                             const double* grad, int* status, cudaStream_t s);
 cudaError_t launch_local_search(const LigandView& L, const double* starts, int n, int max_iters, double tol,
                                 int method, int pair, int partition, int half_mode, double* out_g, double* out_e,
-                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb);
-cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb);
+                                int* out_it, int* out_cv, int* status, cudaStream_t s, int wpb, int cta_warps);
+cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps);
 cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
-                       int* n_launches, cudaEvent_t* ls_events = nullptr);
+                       int cta_warps, int* n_launches, cudaEvent_t* ls_events = nullptr);
 cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s);
 
 // reduce.cu
@@ -34,6 +34,8 @@ cudaError_t launch_reduce4(const float* vecs, int n, int n_red, int method, int 
                            cudaStream_t s);
 cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int half_mode, float* out,
                            cudaStream_t s);
+
+cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 
 // bench_reduce.cu (C2 microbench)
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,

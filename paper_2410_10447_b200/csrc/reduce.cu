@@ -200,7 +200,29 @@ __global__ void reduce7_kernel(const float* __restrict__ recs, int n, int n_red,
   }
 }
 
+// ------------------------------------------------------------ self test
+// ddiv_rn (branch-free division) against the compiler's IEEE div.rn.f64 on
+// counter-generated operands: numerators log-uniform over [2^-40, 2^40]
+// with random sign, denominators log-uniform over [2^-20, 2^40].
+__global__ void ddiv_selftest_kernel(uint64_t seed, long long n, unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t r1 = mix64(seed + 2 * (uint64_t)i + 1), r2 = mix64(seed + 2 * (uint64_t)i + 2);
+    const double m1 = 1.0 + (double)(r1 >> 12) * 0x1p-52, m2 = 1.0 + (double)(r2 >> 12) * 0x1p-52;
+    const int e1 = (int)(r1 & 127) - 40, e2 = (int)((r1 >> 7) & 63) - 20;
+    const double a = ldexp((r2 & 1) ? -m1 : m1, e1), b = ldexp(m2, e2);
+    const double q1 = ddiv_rn(a, b), q2 = a / b;
+    bad += __double_as_longlong(q1) != __double_as_longlong(q2);
+  }
+  atomicAdd(mismatches, bad);
+}
+
 // ------------------------------------------------------------ launchers
+cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s) {
+  ddiv_selftest_kernel<<<148 * 8, 256, 0, s>>>(seed, n, mismatches);
+  return cudaGetLastError();
+}
+
 static int grid_for(size_t n, int block) {
   size_t g = (n + block - 1) / block;
   return (int)(g > 148 * 16 ? 148 * 16 : (g == 0 ? 1 : g));

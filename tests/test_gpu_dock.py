@@ -21,6 +21,7 @@ from paper_2410_10447_b200 import (
     HALF,
     PAIR_FP32,
     PAIR_FP64,
+    PAIR_FP64_FAST,
     SINGLE,
     TCU,
     TCU_SPLIT,
@@ -121,7 +122,8 @@ def test_score_tcu_reference_compatible(dev, port):
                 assert np.all(np.abs(t[i] - wt) <= 2 * half_ulp(wt))
 
 
-@pytest.mark.parametrize("method,pair", [(TCU_SPLIT, PAIR_FP64), (BASELINE, PAIR_FP32), (TCU_SPLIT, PAIR_FP32)])
+@pytest.mark.parametrize("method,pair", [(TCU_SPLIT, PAIR_FP64), (BASELINE, PAIR_FP32), (TCU_SPLIT, PAIR_FP32),
+                                         (BASELINE, PAIR_FP64_FAST), (TCU_SPLIT, PAIR_FP64_FAST)])
 def test_score_within_1e4_of_fp32_reference(method, pair, port, dev):
     dev = Device(0, pair=pair)
     worst_e = worst_g = 0.0
@@ -251,3 +253,29 @@ def test_validate_pair_tcu_vs_baseline(dev, instances):
     assert rep["relative_error"] < 0.002
     rep = validate_pair(dev, instances["s2"], BASELINE, TCU_SPLIT, SINGLE, 100, 12345, LgaSettings())
     assert rep["relative_error"] < 0.002
+
+
+@pytest.mark.parametrize("pair", [PAIR_FP64_FAST, PAIR_FP32])
+def test_fast_modes_cta_local_search_and_lga(pair, port, instances, dev):
+    """Fast pair modes run the CTA-per-pose local search (sites split over 4
+    warps).  Per-evaluation tolerance 1e-4 is covered above; here the search
+    trajectories: final energies within 1e-3 of the CPU reference for >= 90 %
+    of the starts, and LGA paired-seed mean best energy within 0.2 %."""
+    fast = Device(0, pair=pair)
+    inst = instances["synth20"]
+    rng = derive_rng(99, "fast/ls")
+    starts = np.stack([random_pose(rng, inst.n_rot, 0.6) for _ in range(48)])
+    res = fast.local_search_batch(inst, starts, 150, 1e-4, BASELINE, SINGLE, 64)
+    close = 0
+    for s, r in zip(starts, res):
+        w = port.local_search(inst, s, 150, 1e-4, BASELINE, SINGLE, 64)
+        close += abs(r.energy - w["energy"]) <= 1e-3 * max(abs(w["energy"]), 1.0)
+    assert close >= 0.9 * len(starts), close
+    s = LgaSettings()
+    seeds = np.arange(64, dtype=np.uint64) + np.uint64(777)
+    gpu = fast.lga_run_batch(instances["s2"], BASELINE, SINGLE, s, seeds)
+    cpu = [port.lga_run(instances["s2"], BASELINE, SINGLE, s, int(x)) for x in seeds]
+    mg = np.mean([r.best_energy for r in gpu])
+    mc = np.mean([r["best_energy"] for r in cpu])
+    assert abs(mg - mc) / abs(mc) < 0.002
+    fast.close()

@@ -172,3 +172,12 @@ def test_reduce7_all_methods(dev, port):
         s, _ = dev.reduce7_batch(r, TCU_SPLIT, HALF)
         mass = np.abs(r.astype(np.float64)).sum(1)
         assert np.all(np.abs(s - r.astype(np.float64).sum(1)) <= 1e-6 * mass)
+
+
+def test_branch_free_division_is_ieee(dev):
+    """The strict pair loop's ddiv_rn must equal IEEE a / b bit for bit."""
+    import ctypes as C
+
+    bad = C.c_uint64()
+    rc = dev.lib.mdr_selftest_ddiv(dev.ctx, 2024, 200_000_000, C.byref(bad))
+    assert rc == 0 and bad.value == 0, bad.value
