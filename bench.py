@@ -82,39 +82,56 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.window = None
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                          "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(1.0)  # let the sampler come up before the timed region
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
 
+    def mark(self, start: bool):
+        """Bracket the timed region (host wall clock)."""
+        import datetime
+
+        now = datetime.datetime.now()
+        self.window = (now, None) if start else (self.window[0], now)
+
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.2)
             self.proc.terminate()
             self.proc.wait()
             self.f.close()
 
     def summary(self, gpu_index):
+        """Clocks sampled inside the marked timed region."""
+        import datetime
+
         if not self.proc:
             return None
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        lo, hi = self.window if self.window and self.window[1] else (None, None)
         with open(self.path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != gpu_index:
+                if len(parts) < 10 or not parts[1].isdigit() or int(parts[1]) != gpu_index:
                     continue
                 try:
-                    sm.append(float(parts[1]))
-                    mx.append(float(parts[2]))
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                    if lo is not None and not lo <= ts <= hi:
+                        continue
+                    sm.append(float(parts[2]))
+                    mx.append(float(parts[3]))
                 except ValueError:
                     continue
-                for n, v in zip(names, parts[5:9]):
+                for n, v in zip(names, parts[6:10]):
                     if v.lower() == "active":
                         reasons.add(n)
         if not sm:
@@ -271,6 +288,8 @@ def run_gpu_arm(args):
     lib = load()
     pair = {"fp64": PAIR_FP64, "fp32": PAIR_FP32, "fp64fast": PAIR_FP64_FAST}[args.pair]
     dev = Device(local, pair=pair, warps_per_block=args.wpb)
+    if args.cta_warps is not None:
+        assert lib.mdr_ctx_set_cta_warps(dev.ctx, args.cta_warps) == 0
     # a dedicated (non-default) stream shared by torch and the library, so the
     # CUDA events below bracket exactly the library's work
     stream = torch.cuda.Stream(device=local)
@@ -313,12 +332,14 @@ def run_gpu_arm(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(clk_path) as clk:
+        clk.mark(True)
         for k in range(args.steps):
             flush.fill_(float(k))  # > L2 (126 MB): flush between timed steps
             ev[k][0].record(stream)
             step()
             ev[k][1].record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
     if dist:
         dist.barrier()
     launches = dev.launches - launches0
@@ -396,7 +417,7 @@ def run_gpu_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if pair == PAIR_FP64 else "f32",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if pair == PAIR_FP32 else "f64",
             "data": "synthetic (reference random_instance recipe, derive_rng(12345,'synth/small'))",
             "config": {"workload": "C3 small-ligand docking: 100 LGA runs per GPU (BASELINE.json configs[2])",
                        "n_atoms": N_ATOMS, "n_rot": N_ROT, "n_sites": N_SITES, "runs_per_gpu": N_RUNS,
@@ -421,9 +442,46 @@ def run_gpu_arm(args):
         dist.destroy_process_group()
 
 
-def extra_measurements(args, dev, lib, torch):
-    """C2 reduction microbench (ns/call) when the bench kernels are built."""
+def mode_sweep(lib, torch, local, inst, settings, steps=3):
+    """Same docking step under every pair-arithmetic mode and reduction
+    method (device-resident, events on the launching stream)."""
+    from paper_2410_10447_b200 import Device
+
+    stream = torch.cuda.current_stream()
+    seeds = torch.from_numpy((np.arange(N_RUNS, dtype=np.uint64) + np.uint64(1_000_000)).view(np.int64)).to(
+        f"cuda:{local}")
     out = {}
+    for pname, pair in (("fp64", PAIR_FP64), ("fp64fast", PAIR_FP64_FAST), ("fp32", PAIR_FP32)):
+        for mname, method in METHODS.items():
+            if pname != "fp64fast" and mname != "baseline":
+                continue
+            dev = Device(local, pair=pair)
+            dev.set_stream(stream.cuda_stream)
+            di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+            b = lib.mdr_lga_batch_create(dev.ctx, di, method, SINGLE, C.byref(settings), N_RUNS)
+            tot = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+            for _ in range(2):
+                lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+            lib.mdr_lga_batch_total_evals_dev(dev.ctx, b, C.c_void_p(tot.data_ptr()))
+            torch.cuda.synchronize()
+            ev = int(tot.item())
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            for _ in range(steps):
+                lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+            e.record(stream)
+            e.synchronize()
+            ms = s.elapsed_time(e) / steps
+            out[f"{pname}/{mname}"] = {"evals_per_s": ev / (ms * 1e-3), "ms_per_step": ms, "evals_per_step": ev}
+            lib.mdr_lga_batch_destroy(dev.ctx, b)
+            lib.mdr_instance_free(dev.ctx, di)
+            dev.close()
+    return out
+
+
+def extra_measurements(args, dev, lib, torch):
+    """Mode sweep of the docking step + C2 reduction microbench (ns/call)."""
+    out = {"modes": mode_sweep(lib, torch, torch.cuda.current_device(), workload(), LgaSettings())}
     if hasattr(lib, "mdr_reduce_bench_dev"):
         from paper_2410_10447_b200.microbench import reduce_microbench
 
@@ -434,12 +492,14 @@ def extra_measurements(args, dev, lib, torch):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--method", default="baseline", choices=list(METHODS))
-    ap.add_argument("--pair", default="fp64", choices=["fp64", "fp64fast", "fp32"])
+    ap.add_argument("--pair", default="fp64fast", choices=["fp64", "fp64fast", "fp32"],
+                    help="pair-term arithmetic (library default fp64fast; fp64 = reference op order)")
     ap.add_argument("--wpb", type=int, default=2)
+    ap.add_argument("--cta-warps", type=int, default=None, help="warps per pose in fast modes (0 = warp per pose)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", action="store_true", default=True)

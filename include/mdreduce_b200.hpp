@@ -307,8 +307,14 @@ ValidationReport validate_pair(const LigandInstance& instance, ReduceMethod ref_
 namespace b200 {
 // Select the GPU used by the calls above (default 0); one context per thread.
 void set_device(int device);
-// Pair-term arithmetic: true = FP32 fast mode, false = reference FP64 order.
-void set_fast_pairs(bool fp32);
+// Pair-term arithmetic of score / local_search / lga_run (per thread):
+//   Reference — FP64 in the reference's exact operation order;
+//   Fast64    — FP64 with FMA and one reciprocal per pair (default; float
+//               outputs bit-identical to the reference on every case
+//               measured, profiles/r1_parity_report.json);
+//   Fp32      — FP32 pair terms (within 1e-5 relative, fastest).
+enum class PairMode { Reference, Fast64, Fp32 };
+void set_pair_mode(PairMode mode);
 // Many independent evaluations / searches / docking runs in one launch.
 std::vector<ScoreResult> score_batch(const LigandInstance& instance, const std::vector<Genotype>& poses,
                                      ReduceMethod method, AccumMode accum_mode, int partition);

@@ -17,7 +17,7 @@ from . import _lib
 from ._abi import (
     BASELINE,
     HALF,
-    PAIR_FP64,
+    PAIR_FP64_FAST,
     SINGLE,
     TCU,
     TCU_SPLIT,
@@ -70,7 +70,7 @@ class DockResult:
 class Device:
     """One mdr context on one GPU (one CUDA stream)."""
 
-    def __init__(self, device: int = 0, pair: int = PAIR_FP64, warps_per_block: int = 2):
+    def __init__(self, device: int = 0, pair: int = PAIR_FP64_FAST, warps_per_block: int = 2):
         self.lib = _lib.load()
         self.ctx = self.lib.mdr_ctx_create(device)
         if not self.ctx:

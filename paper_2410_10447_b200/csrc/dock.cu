@@ -249,11 +249,12 @@ struct CtaCtx {
   double* g;       // [kMaxDim] current genotype
   double* best;    // [kMaxDim] best genotype
   double* part;    // [W][n_atoms][4] per-warp partial (e, gx, gy, gz)
+  double* world;   // [n_atoms][4] placed atoms of the current pose (x, y, z, w)
   int* ctl;        // [0]: stop flag
 };
 
 __host__ __device__ inline size_t cta_region_bytes(int n_atoms, int warps) {
-  return (size_t)kWarpScratchBytes + 2 * kMaxDim * 8 + (size_t)warps * n_atoms * 32 + 16;
+  return (size_t)kWarpScratchBytes + 2 * kMaxDim * 8 + (size_t)(warps + 1) * n_atoms * 32 + 16;
 }
 
 __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, int warps) {
@@ -263,12 +264,32 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
   c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
   c.best = c.g + kMaxDim;
   c.part = c.best + kMaxDim;
-  c.ctl = reinterpret_cast<int*>(c.part + (size_t)warps * n_atoms * 4);
+  c.world = c.part + (size_t)warps * n_atoms * 4;
+  c.ctl = reinterpret_cast<int*>(c.world + (size_t)n_atoms * 4);
   return c;
 }
 
+// Warp 0: frame of the current genotype and every atom's world position.
+__device__ __forceinline__ Frame cta_place(const SmemLigand& S, const CtaCtx& c) {
+  const int lane = threadIdx.x & 31;
+  const Frame f = build_frame(c.g[3], c.g[4], c.g[5]);
+  const d3 tr = {c.g[0], c.g[1], c.g[2]};
+  for (int i = lane; i < S.n_atoms; i += 32) {
+    const d3 w = atom_world(S, c.g, f.R, tr, i);
+    double* q = c.world + (size_t)i * 4;
+    q[0] = w.x;
+    q[1] = w.y;
+    q[2] = w.z;
+    q[3] = S.atoms[i].w;
+  }
+  return f;
+}
+
 // local_search docking.cpp:310-351 by the whole CTA; the result is valid in
-// warp 0, the best genotype in c.best.
+// warp 0, the best genotype in c.best.  Per evaluation: every warp sums its
+// slice of the sites for all placed atoms (parallel part), then warp 0
+// merges the slices, reduces, projects the gradient, takes the ADADELTA step
+// and places the atoms of the next pose (serial part); two CTA barriers.
 template <int METHOD, int PAIR>
 __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, int max_iters, double tol,
                                      int partition, bool half_mode, const CtaCtx& c) {
@@ -281,6 +302,9 @@ __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, i
     c.best[d] = x;
   }
   __syncthreads();
+  Frame f;
+  if (warp == 0) f = cta_place(S, c);
+  __syncthreads();
   const int j0 = warp * S.n_sites / W, j1 = (warp + 1) * S.n_sites / W;
   double sg0 = 0.0, su0 = 0.0, sg1 = 0.0, su1 = 0.0, hist = 0.0;
   LsResult r;
@@ -289,21 +313,20 @@ __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, i
   r.converged = 0;
   r.status = MDR_OK;
   for (int iter = 0;; ++iter) {
-    const Frame f = build_frame(c.g[3], c.g[4], c.g[5]);
-    const d3 tr = {c.g[0], c.g[1], c.g[2]};
     for (int i = lane; i < S.n_atoms; i += 32) {
-      const d3 world = atom_world(S, c.g, f.R, tr, i);
+      const double* q = c.world + (size_t)i * 4;
       double e = 0.0;
       d3 gg = {0.0, 0.0, 0.0};
-      pair_range<PAIR>(S, world, S.atoms[i].w, j0, j1, e, gg);
-      double* q = c.part + ((size_t)warp * S.n_atoms + i) * 4;
-      q[0] = e;
-      q[1] = gg.x;
-      q[2] = gg.y;
-      q[3] = gg.z;
+      pair_range<PAIR>(S, d3{q[0], q[1], q[2]}, q[3], j0, j1, e, gg);
+      double* o = c.part + ((size_t)warp * S.n_atoms + i) * 4;
+      o[0] = e;
+      o[1] = gg.x;
+      o[2] = gg.y;
+      o[3] = gg.z;
     }
     __syncthreads();
     if (warp == 0) {
+      const d3 tr = {c.g[0], c.g[1], c.g[2]};
       const ScoreOut o = reduce_atoms<METHOD>(S.n_atoms, partition, half_mode, c.ws, [&](int i) {
         Partial p;
         p.e = 0.0;
@@ -313,7 +336,8 @@ __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, i
           p.e += q[0];
           p.g = p.g + d3{q[1], q[2], q[3]};
         }
-        p.t = cross(atom_world(S, c.g, f.R, tr, i) - tr, p.g);
+        const double* q = c.world + (size_t)i * 4;
+        p.t = cross(d3{q[0], q[1], q[2]} - tr, p.g);
         return p;
       });
       const float gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
@@ -354,13 +378,14 @@ __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, i
             adadelta_dim(sg1, su1, x, (double)gr1, lane + 32, rho, eps);
             c.g[lane + 32] = x;
           }
+          __syncwarp();
+          f = cta_place(S, c);  // next pose
         }
       }
       if (lane == 0) c.ctl[0] = done;
     }
     __syncthreads();
     if (c.ctl[0]) break;
-    __syncthreads();  // ctl is rewritten by warp 0 next evaluation
   }
   return r;
 }

@@ -27,7 +27,7 @@ struct Ctx {
 };
 
 thread_local int t_device = 0;
-thread_local bool t_fast = false;
+thread_local int t_pair = MDR_PAIR_FP64_FAST;
 
 mdr_ctx* ctx() {
   thread_local std::unique_ptr<Ctx> holder;
@@ -37,7 +37,7 @@ mdr_ctx* ctx() {
     holder->c = mdr_ctx_create(t_device);
     if (!holder->c) throw DeviceError("mdr_ctx_create failed: no usable CUDA device " + std::to_string(t_device));
   }
-  mdr_ctx_set_pair_precision(holder->c, t_fast ? MDR_PAIR_FP32 : MDR_PAIR_FP64);
+  mdr_ctx_set_pair_precision(holder->c, t_pair);
   return holder->c;
 }
 
@@ -425,7 +425,9 @@ std::array<double, 3> torsion_axis(int k) {  // docking.cpp:181-189
 namespace b200 {
 
 void set_device(int device) { t_device = device; }
-void set_fast_pairs(bool fp32) { t_fast = fp32; }
+void set_pair_mode(PairMode m) {
+  t_pair = m == PairMode::Reference ? MDR_PAIR_FP64 : m == PairMode::Fp32 ? MDR_PAIR_FP32 : MDR_PAIR_FP64_FAST;
+}
 
 std::vector<ScoreResult> score_batch(const LigandInstance& in, const std::vector<Genotype>& poses, ReduceMethod method,
                                      AccumMode accum, int partition) {

@@ -63,3 +63,15 @@ def dev():
     from paper_2410_10447_b200 import Device
 
     return Device(0)
+
+
+@pytest.fixture(scope="session")
+def dev_ref():
+    """A context in MDR_PAIR_FP64: the reference's exact double operation order."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2410_10447_b200 import PAIR_FP64, Device
+
+    return Device(0, pair=PAIR_FP64)
