@@ -43,7 +43,11 @@ def reduce_microbench(dev, lib, torch, blocks=(64, 128, 256), n_red=N_RED, chain
         mass = x_stream[:2048].double().abs().sum(1)
         for k, name in enumerate(names):
             row = {}
-            for mode, x, n, steps in (("chain", x_chain, n_blocks * chain, chain), ("stream", x_stream, n_stream, 0)):
+            modes = (("chain", x_chain, n_blocks * chain, chain), ("stream", x_stream, n_stream, 0))
+            if "tcgen05" in name:  # batched kernel: streaming only
+                modes = modes[1:]
+                row["chain_ns"] = None
+            for mode, x, n, steps in modes:
                 def go():
                     rc = lib.mdr_reduce_bench_dev(dev.ctx, k, B, C.c_void_p(x.data_ptr()), n, steps,
                                                   C.c_void_p(y.data_ptr()))
@@ -93,7 +97,10 @@ def main():
     torch.cuda.set_stream(s)
     if args.kernel >= 0:
         for B in args.blocks:
-            x = torch.rand((args.n // args.chain, B, 4), device="cuda") * 2 - 1
+            if args.chain == 0 or args.kernel == 7:  # streaming mode
+                args.chain = 0
+                args.n = min(args.n, (4 << 30) // (16 * B))
+            x = torch.rand((args.n // max(args.chain, 1), B, 4), device="cuda") * 2 - 1
             y = torch.empty((args.n, 4), device="cuda")
             dev.set_stream(s.cuda_stream)
             lib.mdr_reduce_bench_dev(dev.ctx, args.kernel, B, C.c_void_p(x.data_ptr()), args.n, args.chain,
