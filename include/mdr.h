@@ -245,6 +245,101 @@ int mdr_lga_batch_total_evals_dev(mdr_ctx* ctx, mdr_lga_batch* b, int64_t* d_tot
 int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds,
                               float* ls_ms, float* step_ms, int64_t* ls_evals);
 
+/* ---- grid-map scoring mode (north_star subsystem 1) -------
+ * The reference scores a pose against analytic receptor "sites"
+ * (evaluate_atoms docking.cpp:95-128) and puts AutoDock's grid maps out of
+ * scope.  This mode is the AutoDock-GPU form of the same
+ * operator: per-atom trilinear interpolation of precomputed receptor maps,
+ * intramolecular pair terms between atoms of different rigid groups, and the
+ * exact per-torsion gradient (torque of the moving group about its axis).
+ * Genotype, torsion model (one group per atom, rotate_axis docking.cpp:57-60),
+ * ADADELTA and LGA are the reference's.  Formulas: DESIGN.md §11; CPU
+ * restatement: oracle/mdr_oracle.c (orc_grid_*).  Parity: tolerance (FP32
+ * maps and interpolation), stated in tests/test_gpu_grid.py.
+ *
+ * Energy of a pose (world atom p_i = t + R * rotate_axis(local_i)):
+ *   E = sum_i [ w_i V_type(i)(p_i) + q_i V_elec(p_i) + |q_i| V_desolv(p_i)
+ *               + k_out |p_i - clamp(p_i)|^2 ]
+ *     + sum_{i<j, group_i != group_j} [ eps_ij (rho^12 - 2 rho^6) + k_e q_i q_j / u ]
+ * with V(p) the trilinear interpolation at p clamped into the lattice,
+ * u = r_ij^2 + c2, c2 = 0.5625 d0^2, rho^2 = (d0^2 + c2) / u,
+ * d0 = radius_i + radius_j, eps_ij = sqrt(epsilon_i epsilon_j). */
+/* Outside-lattice restraint k_out (kcal/mol/A^2): an atom beyond the lattice
+ * samples the maps at the clamped point and pays k_out |p - clamp(p)|^2. */
+#define MDR_GRID_OUTSIDE_K 10.0
+
+typedef struct mdr_grid {
+  int32_t nx, ny, nz; /* lattice points per axis (>= 2 each)                */
+  int32_t n_types;    /* atom-type maps; `maps` holds n_types + 2 maps      */
+  double origin[3];   /* world position of lattice point (0, 0, 0)          */
+  double spacing;     /* lattice spacing (Angstrom, > 0)                    */
+  const float* maps;  /* (n_types + 2) x nz x ny x nx, x fastest: the type
+                         maps, then electrostatic, then desolvation          */
+} mdr_grid;
+
+/* Per-atom chemistry of a ligand in grid mode (caller-owned, n_atoms each). */
+typedef struct mdr_ligand_params {
+  const int32_t* atom_type;   /* map index in [0, n_types)                  */
+  const double* atom_charge;  /* q_i                                        */
+  const double* atom_radius;  /* intramolecular d0_ij = radius_i + radius_j */
+  const double* atom_epsilon; /* eps_ij = sqrt(epsilon_i * epsilon_j)       */
+  double elec_scale;          /* k_e (83.0 = 332 / 4, distance-dependent
+                                 dielectric 4r, soft-cored)                 */
+  int32_t intra;              /* 0: no intramolecular term                  */
+  int32_t reserved;
+} mdr_ligand_params;
+
+/* Synthetic receptor maps from the instance's sites (an AutoGrid analogue
+ * for the reference's site model).  At lattice point P, per site j:
+ *   type t : depth_j * depth_scale[t] * (rho^12 - 2 rho^6) with
+ *            d = d0_j * dist_scale[t] (type 0 with scales 1 == the
+ *            reference's analytic well, docking.cpp:113-122)
+ *   elec   : elec_scale * charge_j / (|P - s_j|^2 + 0.5625 d0_j^2)
+ *   desolv : volume_j * exp(-|P - s_j|^2 / (2 sigma^2)). */
+typedef struct mdr_receptor_fields {
+  const double* site_charge;      /* n_sites                                */
+  const double* site_volume;      /* n_sites                                */
+  const double* type_depth_scale; /* n_types                                */
+  const double* type_dist_scale;  /* n_types                                */
+  double elec_scale;
+  double desolv_sigma;
+} mdr_receptor_fields;
+
+typedef struct mdr_dev_grid mdr_dev_grid;
+/* Upload host maps (one device copy, shared by every ligand docked
+ * against this receptor). */
+mdr_dev_grid* mdr_grid_upload(mdr_ctx* ctx, const mdr_grid* grid);
+/* Build the maps on the device from `sites` (uses n_sites / site_xyzdd only);
+ * `shape` gives nx, ny, nz, n_types, origin, spacing (its maps is ignored). */
+mdr_dev_grid* mdr_grid_build(mdr_ctx* ctx, const mdr_instance* sites, const mdr_receptor_fields* fields,
+                             const mdr_grid* shape);
+/* Copy the device maps to host (size (n_types + 2) * nx * ny * nz floats). */
+int mdr_grid_download(mdr_ctx* ctx, const mdr_dev_grid* grid, float* maps);
+void mdr_grid_free(mdr_ctx* ctx, mdr_dev_grid* grid);
+
+/* Switch a device ligand to grid scoring against `grid` (NULL: back to the
+ * analytic site model).  Every _dev call and mdr_lga_batch_create on this
+ * instance then uses the grid kernels (CTA per pose, `partition` threads).
+ * The instance's sites still define the random_genotype box
+ * (docking.cpp:362-374). */
+int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* dinst, const mdr_dev_grid* grid,
+                          const mdr_ligand_params* params);
+
+/* Host-buffer grid-mode calls (ligand uploaded per call, receptor resident).
+ * energy n; gradient n x dim (exact torsion gradient); torque n x 3. */
+int mdr_grid_score_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_instance* inst,
+                         const mdr_ligand_params* params, const double* genotypes, int n, int method,
+                         int partition, float* energy, float* gradient, float* torque);
+int mdr_grid_local_search_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_instance* inst,
+                                const mdr_ligand_params* params, const double* starts, int n, int max_iters,
+                                double convergence_tol, int method, int partition, double* out_genotype,
+                                double* out_energy, int32_t* out_iterations, int32_t* out_converged);
+int mdr_grid_lga_run_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_instance* inst,
+                           const mdr_ligand_params* params, int method, const mdr_lga_settings* settings,
+                           const uint64_t* seeds, int n_runs, double* best_energy, double* best_genotype,
+                           int64_t* evaluations, int32_t* converged, int32_t* n_records,
+                           mdr_ls_record* records);
+
 #ifdef __cplusplus
 }
 #endif

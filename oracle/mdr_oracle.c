@@ -530,33 +530,48 @@ static void scale_add_stats(mdr_sync_stats* acc, const mdr_sync_stats* one, uint
   acc->precision_conversions += k * one->precision_conversions;
 }
 
-/* local_search docking.cpp:310-351 */
-int orc_local_search(const mdr_instance* in, const double* start, int max_iters, double tol,
-                     int method, int accum, int partition, double* out_g, double* out_e,
-                     int32_t* out_iters, int32_t* out_conv, mdr_sync_stats* st) {
+/* A scorer: energy + gradient of genotype g (double views of whatever the
+ * scoring path returns; the analytic path returns the reference's floats). */
+typedef int (*orc_scorefn)(const void* sctx, const double* g, double* e, double* grad);
+
+typedef struct {
+  const mdr_instance* in;
+  int method, accum, partition;
+} analytic_sctx;
+
+static int analytic_score(const void* sctx, const double* g, double* e, double* grad) {
+  const analytic_sctx* a = (const analytic_sctx*)sctx;
+  float ef, tq[3], gr[64];
+  const int rc = orc_score(a->in, g, a->method, a->accum, a->partition, &ef, gr, tq, NULL);
+  if (rc) return rc;
+  *e = ef;
+  for (int d = 0; d < 6 + a->in->n_rot; ++d) grad[d] = gr[d];
+  return MDR_OK;
+}
+
+/* local_search docking.cpp:310-351 over any scorer */
+static int ls_core(orc_scorefn fn, const void* sctx, int dim, const double* start, int max_iters, double tol,
+                   double* out_g, double* out_e, int32_t* out_iters, int32_t* out_conv) {
   enum { WINDOW = 16 };
-  const int dim = 6 + in->n_rot;
   double* g = (double*)malloc(sizeof(double) * (size_t)dim);
   double* sg = (double*)calloc((size_t)dim, sizeof(double));
   double* su = (double*)calloc((size_t)dim, sizeof(double));
   double* gd = (double*)malloc(sizeof(double) * (size_t)dim);
-  float* gr = (float*)malloc(sizeof(float) * (size_t)dim);
   double* hist = (double*)malloc(sizeof(double) * (size_t)(max_iters + 1));
   memcpy(g, start, sizeof(double) * (size_t)dim);
   normalize_angles(g, dim);
-  float e, tq[3];
-  int rc = orc_score(in, g, method, accum, partition, &e, gr, tq, NULL);
+  double e;
+  int rc = fn(sctx, g, &e, gd);
   int iters = 0, conv = 0;
   double best = e;
   memcpy(out_g, g, sizeof(double) * (size_t)dim);
   hist[0] = best;
   for (int it = 1; rc == MDR_OK && it <= max_iters; ++it) {
-    for (int d = 0; d < dim; ++d) gd[d] = gr[d];
     rc = orc_adadelta_step(dim, 0.95, 1e-6, sg, su, g, gd);
     if (rc) break;
-    rc = orc_score(in, g, method, accum, partition, &e, gr, tq, NULL);
+    rc = fn(sctx, g, &e, gd);
     if (rc) break;
-    if ((double)e < best) {
+    if (e < best) {
       best = e;
       memcpy(out_g, g, sizeof(double) * (size_t)dim);
     }
@@ -570,13 +585,23 @@ int orc_local_search(const mdr_instance* in, const double* start, int max_iters,
   *out_e = best;
   *out_iters = iters;
   *out_conv = conv;
+  free(g); free(sg); free(su); free(gd); free(hist);
+  return rc;
+}
+
+int orc_local_search(const mdr_instance* in, const double* start, int max_iters, double tol,
+                     int method, int accum, int partition, double* out_g, double* out_e,
+                     int32_t* out_iters, int32_t* out_conv, mdr_sync_stats* st) {
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  const analytic_sctx a = {in, method, accum, partition};
+  const int rc = ls_core(analytic_score, &a, 6 + in->n_rot, start, max_iters, tol, out_g, out_e, out_iters,
+                         out_conv);
   if (st) {
     mdr_sync_stats one;
     score_stats(method, accum, partition, &one);
     zero_stats(st);
-    scale_add_stats(st, &one, (uint64_t)iters + 1);
+    scale_add_stats(st, &one, (uint64_t)*out_iters + 1);
   }
-  free(g); free(sg); free(su); free(gd); free(gr); free(hist);
   return rc;
 }
 
@@ -604,11 +629,9 @@ int orc_lga_max_records(const mdr_lga_settings* s) {
 }
 
 /* lga_run docking.cpp:392-517 */
-int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_settings* s,
-                uint64_t seed, double* best_e, double* best_g, int64_t* evals_out, int32_t* conv,
-                int32_t* n_records, mdr_ls_record* records, int max_records, mdr_sync_stats* st) {
-  if (s->population_size < 2) return MDR_ERR_SIZE;
-  if (!partition_ok(s->partition, method)) return MDR_ERR_BLOCK_SIZE;
+static int lga_core(orc_scorefn fn, const void* sctx, const mdr_instance* in, const mdr_lga_settings* s,
+                    uint64_t seed, double* best_e, double* best_g, int64_t* evals_out, int32_t* conv,
+                    int32_t* n_records, mdr_ls_record* records, int max_records) {
   const int dim = 6 + in->n_rot, P = s->population_size;
   orc_rng r = orc_rng_make(seed, "lga");
   double* pop = (double*)malloc(sizeof(double) * (size_t)(P * dim));
@@ -616,9 +639,9 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
   double* pe = (double*)malloc(sizeof(double) * (size_t)P);
   double* ne = (double*)malloc(sizeof(double) * (size_t)P);
   int* order = (int*)malloc(sizeof(int) * (size_t)P);
-  float* gr = (float*)malloc(sizeof(float) * (size_t)dim);
+  double* gr = (double*)malloc(sizeof(double) * (size_t)dim);
   double* lsg = (double*)malloc(sizeof(double) * (size_t)dim);
-  float e, tq[3];
+  double e;
   int64_t evals = 0;
   int nrec = 0, rc = MDR_OK;
   double best = DBL_MAX;
@@ -641,7 +664,7 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
   } while (0)
   for (int p = 0; p < P; ++p) {
     random_genotype(in, &r, pop + p * dim);
-    rc = orc_score(in, pop + p * dim, method, accum, s->partition, &e, gr, tq, NULL);
+    rc = fn(sctx, pop + p * dim, &e, gr);
     if (rc) goto done;
     ++evals;
     pe[p] = e;
@@ -670,7 +693,7 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
         }
         for (int d = 0; d < dim; ++d) ch[d] = ch[d] + s->mutation_sigma * orc_normal(&r);
         normalize_angles(ch, dim);
-        rc = orc_score(in, ch, method, accum, s->partition, &e, gr, tq, NULL);
+        rc = fn(sctx, ch, &e, gr);
         if (rc) goto done;
         ++evals;
         ne[1 + i] = e;
@@ -691,8 +714,8 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
         const int t = order[q];
         double le;
         int32_t it, cv;
-        rc = orc_local_search(in, nxt + t * dim, s->ls_max_iters, s->ls_convergence_tol, method,
-                              accum, s->partition, lsg, &le, &it, &cv, NULL);
+        rc = ls_core(fn, sctx, dim, nxt + t * dim, s->ls_max_iters, s->ls_convergence_tol, lsg, &le, &it,
+                     &cv);
         if (rc) goto done;
         evals += it + 1;
         memcpy(nxt + t * dim, lsg, sizeof(double) * (size_t)dim);
@@ -713,8 +736,7 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
       memcpy(lsg, best_g, sizeof(double) * (size_t)dim);
       double* start = (double*)malloc(sizeof(double) * (size_t)dim);
       memcpy(start, best_g, sizeof(double) * (size_t)dim);
-      rc = orc_local_search(in, start, iters, s->ls_convergence_tol, method, accum, s->partition,
-                            lsg, &le, &it, &cv, NULL);
+      rc = ls_core(fn, sctx, dim, start, iters, s->ls_convergence_tol, lsg, &le, &it, &cv);
       free(start);
       if (rc) goto done;
       evals += it + 1;
@@ -729,14 +751,231 @@ done:
   *best_e = best;
   *evals_out = evals;
   *n_records = nrec;
-  if (st) {
-    mdr_sync_stats one;
-    score_stats(method, accum, s->partition, &one);
-    zero_stats(st);
-    scale_add_stats(st, &one, (uint64_t)evals);
-  }
 #undef TRACK
 #undef RECORD
   free(pop); free(nxt); free(pe); free(ne); free(order); free(gr); free(lsg);
   return rc;
+}
+
+int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_settings* s,
+                uint64_t seed, double* best_e, double* best_g, int64_t* evals_out, int32_t* conv,
+                int32_t* n_records, mdr_ls_record* records, int max_records, mdr_sync_stats* st) {
+  if (s->population_size < 2) return MDR_ERR_SIZE;
+  if (!partition_ok(s->partition, method)) return MDR_ERR_BLOCK_SIZE;
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  const analytic_sctx a = {in, method, accum, s->partition};
+  const int rc = lga_core(analytic_score, &a, in, s, seed, best_e, best_g, evals_out, conv, n_records, records,
+                          max_records);
+  if (st) {
+    mdr_sync_stats one;
+    score_stats(method, accum, s->partition, &one);
+    zero_stats(st);
+    scale_add_stats(st, &one, (uint64_t)*evals_out);
+  }
+  return rc;
+}
+
+/* ================================================================ grid mode
+ * CPU restatement of the grid-map scoring mode (include/mdr.h "grid-map
+ * scoring mode").  There is no reference implementation of
+ * this path (SPEC.md:425 puts grid maps out of scope): the formulas are
+ * AutoDock-GPU's (trilinear map interpolation, intramolecular pairs, per-
+ * rotatable-bond torque) restated on the reference's genotype and torsion
+ * model (build_frame docking.cpp:78-91, rotate_axis :57-60, the soft-core
+ * well :113-122, the projection :217-231 with exact per-group torque as in
+ * score_reference :244-268).  Everything here is double precision; the
+ * device path computes in FP32 on FP32 maps (tolerance parity). */
+
+/* receptor map builder (mdr_grid_build) */
+int orc_grid_build(const mdr_instance* sites, const mdr_receptor_fields* F, const mdr_grid* shape, float* maps) {
+  const int nx = shape->nx, ny = shape->ny, nz = shape->nz, nt = shape->n_types;
+  const size_t stride = (size_t)nx * ny * nz;
+  const double two_s2 = 2.0 * F->desolv_sigma * F->desolv_sigma;
+  for (int iz = 0; iz < nz; ++iz)
+    for (int iy = 0; iy < ny; ++iy)
+      for (int ix = 0; ix < nx; ++ix) {
+        const double P[3] = {shape->origin[0] + shape->spacing * ix, shape->origin[1] + shape->spacing * iy,
+                             shape->origin[2] + shape->spacing * iz};
+        const size_t o = ((size_t)iz * ny + iy) * nx + ix;
+        for (int t = 0; t < nt + 2; ++t) {
+          double v = 0.0;
+          for (int j = 0; j < sites->n_sites; ++j) {
+            const double* s = sites->site_xyzdd + 5 * j;
+            const double dx = P[0] - s[0], dy = P[1] - s[1], dz = P[2] - s[2];
+            const double r2 = dx * dx + dy * dy + dz * dz;
+            if (t < nt) {
+              const double d = s[4] * F->type_dist_scale[t];
+              const double c2 = 0.5625 * d * d;
+              const double u = r2 + c2;
+              const double rho2 = (d * d + c2) / u;
+              const double rho6 = rho2 * rho2 * rho2;
+              const double rho12 = rho6 * rho6;
+              v += s[3] * F->type_depth_scale[t] * (rho12 - 2.0 * rho6);
+            } else if (t == nt) {
+              v += F->elec_scale * F->site_charge[j] / (r2 + 0.5625 * s[4] * s[4]);
+            } else {
+              v += F->site_volume[j] * exp(-r2 / two_s2);
+            }
+          }
+          maps[(size_t)t * stride + o] = (float)v;
+        }
+      }
+  return MDR_OK;
+}
+
+typedef struct {
+  const mdr_instance* in;
+  const mdr_grid* G;
+  const mdr_ligand_params* P;
+} grid_sctx;
+
+/* Trilinear interpolation of the atom's combined map c = w*type + q*elec +
+ * |q|*desolv at world point p; returns V, dV/dp (clamped axes: 0) and the
+ * outside-lattice offset d = p - clamp(p). */
+static double grid_sample(const mdr_grid* G, int type, double w, double q, const double p[3], double dvdp[3],
+                          double off[3]) {
+  const int n[3] = {G->nx, G->ny, G->nz};
+  int i0[3];
+  double f[3];
+  int inside[3];
+  for (int a = 0; a < 3; ++a) {
+    const double gc = (p[a] - G->origin[a]) / G->spacing;
+    double gcc = gc < 0.0 ? 0.0 : gc;
+    gcc = gcc > (double)(n[a] - 1) ? (double)(n[a] - 1) : gcc;
+    int i = (int)floor(gcc);
+    if (i > n[a] - 2) i = n[a] - 2;
+    i0[a] = i;
+    f[a] = gcc - i;
+    inside[a] = gc >= 0.0 && gc <= (double)(n[a] - 1);
+    off[a] = G->spacing * (gc - gcc);
+  }
+  const size_t stride = (size_t)G->nx * G->ny * G->nz;
+  const float* mt = G->maps + (size_t)type * stride;
+  const float* me = G->maps + (size_t)G->n_types * stride;
+  const float* md = me + stride;
+  const double aq = fabs(q);
+  double c[2][2][2];
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const size_t o = ((size_t)(i0[2] + dz) * G->ny + (i0[1] + dy)) * G->nx + (i0[0] + dx);
+        c[dz][dy][dx] = w * mt[o] + q * me[o] + aq * md[o];
+      }
+  /* x pass, y pass, z pass: value and derivatives w.r.t. the fractions */
+  double vx[2][2], gx[2][2];
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy) {
+      gx[dz][dy] = c[dz][dy][1] - c[dz][dy][0];
+      vx[dz][dy] = c[dz][dy][0] + f[0] * gx[dz][dy];
+    }
+  double vy[2], gxy[2], gyy[2];
+  for (int dz = 0; dz < 2; ++dz) {
+    gyy[dz] = vx[dz][1] - vx[dz][0];
+    vy[dz] = vx[dz][0] + f[1] * gyy[dz];
+    gxy[dz] = gx[dz][0] + f[1] * (gx[dz][1] - gx[dz][0]);
+  }
+  const double v = vy[0] + f[2] * (vy[1] - vy[0]);
+  const double dfx = gxy[0] + f[2] * (gxy[1] - gxy[0]);
+  const double dfy = gyy[0] + f[2] * (gyy[1] - gyy[0]);
+  const double dfz = vy[1] - vy[0];
+  dvdp[0] = inside[0] ? dfx / G->spacing : 0.0;
+  dvdp[1] = inside[1] ? dfy / G->spacing : 0.0;
+  dvdp[2] = inside[2] ? dfz / G->spacing : 0.0;
+  return v;
+}
+
+int orc_grid_score(const mdr_instance* in, const mdr_grid* G, const mdr_ligand_params* P, const double* g,
+                   double* energy, double* grad, double* torque, double* e_intra_out) {
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  frame_t f;
+  v3 tw[64];
+  f.tors_world = tw;
+  build_frame(in, g, &f);
+  const int na = in->n_atoms;
+  v3* r = (v3*)malloc(sizeof(v3) * (size_t)na);
+  v3* F = (v3*)calloc((size_t)na, sizeof(v3));
+  v3* Fi = (v3*)calloc((size_t)na, sizeof(v3));
+  const v3 t = {{g[0], g[1], g[2]}};
+  double e_inter = 0.0, e_intra = 0.0;
+  v3 gs = {{0, 0, 0}}, ts = {{0, 0, 0}};
+  for (int i = 0; i < na; ++i) {
+    const double* at = in->atom_xyzw + 4 * i;
+    v3 local = {{at[0], at[1], at[2]}};
+    const int k = in->atom_torsion[i];
+    if (k >= 0) {
+      const v3 ax = orc_torsion_axis(k);
+      const double ang = g[6 + k], c = cos(ang), s = sin(ang);
+      local = add3(add3(scl3(c, local), scl3(s, cross3(ax, local))), scl3((1.0 - c) * dot3(ax, local), ax));
+    }
+    r[i] = mv3(&f.R, local);
+    const v3 world = add3(t, r[i]);
+    double dv[3], off[3];
+    const double q = P->atom_charge[i];
+    double e = grid_sample(G, P->atom_type[i], at[3], q, world.v, dv, off);
+    for (int a = 0; a < 3; ++a) {
+      e += MDR_GRID_OUTSIDE_K * off[a] * off[a];
+      F[i].v[a] = dv[a] + 2.0 * MDR_GRID_OUTSIDE_K * off[a];
+    }
+    e_inter += e;
+    gs = add3(gs, F[i]);
+    ts = add3(ts, cross3(r[i], F[i]));
+  }
+  if (P->intra) {
+    for (int i = 0; i < na; ++i)
+      for (int j = i + 1; j < na; ++j) {
+        if (in->atom_torsion[i] == in->atom_torsion[j]) continue;
+        const v3 d = sub3(r[i], r[j]);
+        const double d0 = P->atom_radius[i] + P->atom_radius[j];
+        const double c2 = 0.5625 * d0 * d0;
+        const double u = dot3(d, d) + c2;
+        const double rho2 = (d0 * d0 + c2) / u;
+        const double rho6 = rho2 * rho2 * rho2;
+        const double rho12 = rho6 * rho6;
+        const double eps = sqrt(P->atom_epsilon[i] * P->atom_epsilon[j]);
+        const double qq = P->elec_scale * P->atom_charge[i] * P->atom_charge[j];
+        e_intra += eps * (rho12 - 2.0 * rho6) + qq / u;
+        const double sc = -12.0 * eps * (rho12 - rho6) / u - 2.0 * qq / (u * u);
+        Fi[i] = add3(Fi[i], scl3(sc, d));
+        Fi[j] = sub3(Fi[j], scl3(sc, d));
+      }
+  }
+  *energy = e_inter + e_intra;
+  if (e_intra_out) *e_intra_out = e_intra;
+  torque[0] = ts.v[0]; torque[1] = ts.v[1]; torque[2] = ts.v[2];
+  grad[0] = gs.v[0]; grad[1] = gs.v[1]; grad[2] = gs.v[2];
+  grad[3] = dot3(f.ax_phi, ts);
+  grad[4] = dot3(f.ax_theta, ts);
+  grad[5] = dot3(f.ax_alpha, ts);
+  for (int k = 0; k < in->n_rot; ++k) {
+    v3 tk = {{0, 0, 0}};
+    for (int i = 0; i < na; ++i)
+      if (in->atom_torsion[i] == k) tk = add3(tk, cross3(r[i], add3(F[i], Fi[i])));
+    grad[6 + k] = dot3(tw[k], tk);
+  }
+  free(r); free(F); free(Fi);
+  return MDR_OK;
+}
+
+static int grid_score_fn(const void* sctx, const double* g, double* e, double* grad) {
+  const grid_sctx* c = (const grid_sctx*)sctx;
+  double tq[3];
+  return orc_grid_score(c->in, c->G, c->P, g, e, grad, tq, NULL);
+}
+
+int orc_grid_local_search(const mdr_instance* in, const mdr_grid* G, const mdr_ligand_params* P,
+                          const double* start, int max_iters, double tol, double* out_g, double* out_e,
+                          int32_t* out_iters, int32_t* out_conv) {
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  const grid_sctx c = {in, G, P};
+  return ls_core(grid_score_fn, &c, 6 + in->n_rot, start, max_iters, tol, out_g, out_e, out_iters, out_conv);
+}
+
+int orc_grid_lga_run(const mdr_instance* in, const mdr_grid* G, const mdr_ligand_params* P,
+                     const mdr_lga_settings* s, uint64_t seed, double* best_e, double* best_g, int64_t* evals_out,
+                     int32_t* conv, int32_t* n_records, mdr_ls_record* records, int max_records) {
+  if (s->population_size < 2) return MDR_ERR_SIZE;
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  const grid_sctx c = {in, G, P};
+  return lga_core(grid_score_fn, &c, in, s, seed, best_e, best_g, evals_out, conv, n_records, records,
+                  max_records);
 }

@@ -20,6 +20,7 @@ import numpy as np
 
 from paper_2410_10447_b200._abi import (
     BASELINE,
+    Grid,
     LgaSettings,
     LsRecord,
     SyncStats,
@@ -222,3 +223,46 @@ class Oracle:
                 for i in range(min(nr.value, maxr))]
         return dict(best_energy=be.value, best_genotype=g, evaluations=ev.value,
                     converged=bool(cv.value), runs=runs, total_stats=st)
+
+    # ---- grid mode (port only; no reference counterpart) -------------------
+    def grid_build(self, sites_inst, fields, grid: Grid) -> np.ndarray:
+        maps = np.zeros((grid.n_types + 2,) + tuple(int(v) for v in grid.shape[::-1]), np.float32)
+        shape = grid.c()
+        self._chk(self.lib.orc_grid_build(sites_inst.cref(), fields.cref(), C.byref(shape), fptr(maps)))
+        return maps
+
+    def grid_score(self, inst, grid: Grid, params, g):
+        g = np.ascontiguousarray(g, np.float64)
+        e, ei = C.c_double(), C.c_double()
+        grad = np.zeros(inst.dim)
+        tq = np.zeros(3)
+        cg = grid.c()
+        self._chk(self.lib.orc_grid_score(inst.cref(), C.byref(cg), params.cref(), dptr(g), C.byref(e),
+                                          dptr(grad), dptr(tq), C.byref(ei)))
+        return e.value, grad, tq, ei.value
+
+    def grid_local_search(self, inst, grid: Grid, params, start, max_iters, tol):
+        f = self.lib.orc_grid_local_search
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_double,
+                      C.POINTER(C.c_double), C.c_void_p, C.c_void_p, C.c_void_p]
+        start = np.ascontiguousarray(start, np.float64)
+        g = np.zeros(inst.dim)
+        e, it, cv = C.c_double(), C.c_int32(), C.c_int32()
+        cg = grid.c()
+        self._chk(f(inst.cref(), C.byref(cg), params.cref(), dptr(start), max_iters, tol, dptr(g), C.byref(e),
+                    C.byref(it), C.byref(cv)))
+        return dict(genotype=g, energy=e.value, iterations=it.value, converged=bool(cv.value))
+
+    def grid_lga_run(self, inst, grid: Grid, params, settings: LgaSettings, seed: int):
+        maxr = settings.max_records
+        g = np.zeros(inst.dim)
+        be, ev, cv, nr = C.c_double(), C.c_int64(), C.c_int32(), C.c_int32()
+        recs = (LsRecord * maxr)()
+        cg = grid.c()
+        self._chk(self.lib.orc_grid_lga_run(inst.cref(), C.byref(cg), params.cref(), C.byref(settings),
+                                            C.c_uint64(seed), C.byref(be), dptr(g), C.byref(ev), C.byref(cv),
+                                            C.byref(nr), recs, maxr))
+        runs = [(recs[i].best_energy, recs[i].iterations, bool(recs[i].converged))
+                for i in range(min(nr.value, maxr))]
+        return dict(best_energy=be.value, best_genotype=g, evaluations=ev.value, converged=bool(cv.value),
+                    runs=runs)

@@ -371,3 +371,164 @@ def random_pose(rng: RngStream, nrot: int, spread: float) -> np.ndarray:
     g += [rng.uniform(-3.1, 3.1) for _ in range(3)]
     g += [rng.uniform(-3.1, 3.1) for _ in range(nrot)]
     return np.array(g)
+
+
+# ----------------------------------------------------------------- grid mode
+# mdr.h "grid-map scoring mode".
+GRID_OUTSIDE_K = 10.0  # MDR_GRID_OUTSIDE_K
+
+
+class CGrid(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("n_types", C.c_int32),
+        ("origin", C.c_double * 3), ("spacing", C.c_double),
+        ("maps", C.POINTER(C.c_float)),
+    ]
+
+
+class CLigandParams(C.Structure):
+    _fields_ = [
+        ("atom_type", C.POINTER(C.c_int32)), ("atom_charge", C.POINTER(C.c_double)),
+        ("atom_radius", C.POINTER(C.c_double)), ("atom_epsilon", C.POINTER(C.c_double)),
+        ("elec_scale", C.c_double), ("intra", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class CReceptorFields(C.Structure):
+    _fields_ = [
+        ("site_charge", C.POINTER(C.c_double)), ("site_volume", C.POINTER(C.c_double)),
+        ("type_depth_scale", C.POINTER(C.c_double)), ("type_dist_scale", C.POINTER(C.c_double)),
+        ("elec_scale", C.c_double), ("desolv_sigma", C.c_double),
+    ]
+
+
+@dataclass
+class Grid:
+    """Receptor maps: (n_types + 2, nz, ny, nx) float32 (types, elec, desolv)."""
+
+    shape: tuple  # (nx, ny, nz)
+    n_types: int
+    origin: tuple
+    spacing: float
+    maps: np.ndarray | None = None
+    _c: CGrid | None = field(default=None, repr=False, compare=False)
+
+    def c(self) -> CGrid:
+        g = CGrid()
+        g.nx, g.ny, g.nz = (int(v) for v in self.shape)
+        g.n_types = int(self.n_types)
+        g.origin = (C.c_double * 3)(*[float(v) for v in self.origin])
+        g.spacing = float(self.spacing)
+        if self.maps is not None:
+            self.maps = np.ascontiguousarray(self.maps, np.float32)
+            g.maps = fptr(self.maps)
+        self._c = g
+        return g
+
+    def cref(self):
+        return C.byref(self.c())
+
+    @property
+    def n_points(self) -> int:
+        nx, ny, nz = self.shape
+        return int(nx) * int(ny) * int(nz)
+
+
+@dataclass
+class LigandParams:
+    """Per-atom chemistry for grid mode (mdr_ligand_params)."""
+
+    atom_type: np.ndarray
+    charge: np.ndarray
+    radius: np.ndarray
+    epsilon: np.ndarray
+    elec_scale: float = 83.0
+    intra: bool = True
+    _c: CLigandParams | None = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.atom_type = np.ascontiguousarray(self.atom_type, np.int32)
+        self.charge = np.ascontiguousarray(self.charge, np.float64)
+        self.radius = np.ascontiguousarray(self.radius, np.float64)
+        self.epsilon = np.ascontiguousarray(self.epsilon, np.float64)
+
+    def c(self) -> CLigandParams:
+        p = CLigandParams()
+        p.atom_type = i32ptr(self.atom_type)
+        p.atom_charge = dptr(self.charge)
+        p.atom_radius = dptr(self.radius)
+        p.atom_epsilon = dptr(self.epsilon)
+        p.elec_scale = float(self.elec_scale)
+        p.intra = 1 if self.intra else 0
+        self._c = p
+        return p
+
+    def cref(self):
+        return C.byref(self.c())
+
+
+@dataclass
+class ReceptorFields:
+    """Inputs of the synthetic map builder (mdr_receptor_fields)."""
+
+    site_charge: np.ndarray
+    site_volume: np.ndarray
+    type_depth_scale: np.ndarray
+    type_dist_scale: np.ndarray
+    elec_scale: float = 83.0
+    desolv_sigma: float = 3.6
+    _c: CReceptorFields | None = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        for k in ("site_charge", "site_volume", "type_depth_scale", "type_dist_scale"):
+            setattr(self, k, np.ascontiguousarray(getattr(self, k), np.float64))
+
+    @property
+    def n_types(self) -> int:
+        return int(self.type_depth_scale.size)
+
+    def c(self) -> CReceptorFields:
+        f = CReceptorFields()
+        f.site_charge = dptr(self.site_charge)
+        f.site_volume = dptr(self.site_volume)
+        f.type_depth_scale = dptr(self.type_depth_scale)
+        f.type_dist_scale = dptr(self.type_dist_scale)
+        f.elec_scale = float(self.elec_scale)
+        f.desolv_sigma = float(self.desolv_sigma)
+        self._c = f
+        return f
+
+    def cref(self):
+        return C.byref(self.c())
+
+
+def random_ligand_params(rng: RngStream, n_atoms: int, n_types: int) -> LigandParams:
+    """Synthetic ligand chemistry: per atom, in this draw order,
+    type = next_index(n_types), charge U(-0.4, 0.4), radius U(0.35, 0.55),
+    epsilon U(0.02, 0.1)."""
+    t, q, r, e = [], [], [], []
+    for _ in range(n_atoms):
+        t.append(rng.next_index(n_types))
+        q.append(rng.uniform(-0.4, 0.4))
+        r.append(rng.uniform(0.35, 0.55))
+        e.append(rng.uniform(0.02, 0.1))
+    return LigandParams(np.array(t), np.array(q), np.array(r), np.array(e))
+
+
+def random_receptor_fields(rng: RngStream, n_sites: int, n_types: int) -> ReceptorFields:
+    """Synthetic receptor chemistry: per site charge U(-0.5, 0.5) and volume
+    U(0.5, 1.5); type 0 has scales (1, 1) (== the reference's analytic well),
+    type t > 0 depth scale U(0.5, 1.5) and distance scale U(0.8, 1.2)."""
+    q = [rng.uniform(-0.5, 0.5) for _ in range(n_sites)]
+    v = [rng.uniform(0.5, 1.5) for _ in range(n_sites)]
+    ds, dd = [1.0], [1.0]
+    for _ in range(1, n_types):
+        ds.append(rng.uniform(0.5, 1.5))
+        dd.append(rng.uniform(0.8, 1.2))
+    return ReceptorFields(np.array(q), np.array(v), np.array(ds), np.array(dd))
+
+
+def centered_grid(n: int, spacing: float, n_types: int, center=(0.0, 0.0, 0.0)) -> Grid:
+    """An n^3 lattice centred on `center` (C4: n=126, spacing 0.375)."""
+    half = 0.5 * (n - 1) * spacing
+    return Grid((n, n, n), n_types, tuple(c - half for c in center), spacing)

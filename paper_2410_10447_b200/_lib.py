@@ -61,6 +61,14 @@ _SIGS = {
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
+    "mdr_grid_upload": (P, [P, P]),
+    "mdr_grid_build": (P, [P, P, P, P]),
+    "mdr_grid_download": (I, [P, P, P]),
+    "mdr_grid_free": (None, [P, P]),
+    "mdr_instance_set_grid": (I, [P, P, P, P]),
+    "mdr_grid_score_batch": (I, [P, P, P, P, P, I, I, I, P, P, P]),
+    "mdr_grid_local_search_batch": (I, [P, P, P, P, P, I, I, D, I, I, P, P, P, P]),
+    "mdr_grid_lga_run_batch": (I, [P, P, P, P, I, P, P, I, P, P, P, P, P, P]),
 }
 
 # Optional entry points (present once their module is built).
@@ -69,7 +77,6 @@ _OPTIONAL = {
     "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
     "mdr_tc05_reduce4_dev": (I, [P, P, I, I, P]),
-    "mdr_grid_build_dev": (I, []),
 }
 
 

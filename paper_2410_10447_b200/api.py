@@ -21,8 +21,11 @@ from ._abi import (
     SINGLE,
     TCU,
     TCU_SPLIT,
+    Grid,
     Instance,
     LgaSettings,
+    LigandParams,
+    ReceptorFields,
     LsRecord,
     SizeError,
     SyncStats,
@@ -286,6 +289,92 @@ class Device:
 
     def lga_run(self, inst, method, accum, settings: LgaSettings, seed: int) -> DockResult:
         return self.lga_run_batch(inst, method, accum, settings, [seed])[0]
+
+    # ------------------------------------------------- grid-map mode (§8 f1)
+    # include/mdr.h "grid-map scoring mode": partition = CTA threads per pose
+    # (>= 6 + n_rot); accum does not apply (fp32 / tf32 reductions).
+    def grid_upload(self, grid: Grid) -> DevGrid:
+        h = self.lib.mdr_grid_upload(self.ctx, grid.cref())
+        if not h:
+            raise_for(6, self.lib.mdr_last_error(self.ctx).decode())
+        return DevGrid(self, h, grid)
+
+    def grid_build(self, sites: Instance, fields: ReceptorFields, grid: Grid) -> DevGrid:
+        h = self.lib.mdr_grid_build(self.ctx, sites.cref(), fields.cref(), grid.cref())
+        if not h:
+            raise_for(6, self.lib.mdr_last_error(self.ctx).decode())
+        return DevGrid(self, h, grid)
+
+    def grid_score_batch(self, dgrid: DevGrid, inst: Instance, params: LigandParams, genotypes, method=BASELINE,
+                         partition=64):
+        g = np.ascontiguousarray(genotypes, np.float64).reshape(-1, inst.dim)
+        n = g.shape[0]
+        e = np.zeros(n, np.float32)
+        grad = np.zeros((n, inst.dim), np.float32)
+        tq = np.zeros((n, 3), np.float32)
+        self._chk(self.lib.mdr_grid_score_batch(self.ctx, dgrid.h, inst.cref(), params.cref(), _p(g), n, method,
+                                                partition, _p(e), _p(grad), _p(tq)))
+        return e, grad, tq
+
+    def grid_local_search_batch(self, dgrid: DevGrid, inst: Instance, params: LigandParams, starts, max_iters, tol,
+                                method=BASELINE, partition=64):
+        s = np.ascontiguousarray(starts, np.float64).reshape(-1, inst.dim)
+        n = s.shape[0]
+        g = np.zeros((n, inst.dim))
+        e = np.zeros(n)
+        it = np.zeros(n, np.int32)
+        cv = np.zeros(n, np.int32)
+        self._chk(self.lib.mdr_grid_local_search_batch(self.ctx, dgrid.h, inst.cref(), params.cref(), _p(s), n,
+                                                       max_iters, tol, method, partition, _p(g), _p(e), _p(it),
+                                                       _p(cv)))
+        return [LocalSearchResult(g[i], float(e[i]), int(it[i]), bool(cv[i]), SyncStats()) for i in range(n)]
+
+    def grid_lga_run_batch(self, dgrid: DevGrid, inst: Instance, params: LigandParams, method,
+                           settings: LgaSettings, seeds):
+        seeds = np.ascontiguousarray(seeds, np.uint64).reshape(-1)
+        n = seeds.size
+        maxr = settings.max_records
+        be = np.zeros(n)
+        bg = np.zeros((n, inst.dim))
+        ev = np.zeros(n, np.int64)
+        cv = np.zeros(n, np.int32)
+        nr = np.zeros(n, np.int32)
+        recs = (LsRecord * (n * maxr))()
+        self._chk(self.lib.mdr_grid_lga_run_batch(self.ctx, dgrid.h, inst.cref(), params.cref(), method,
+                                                  C.byref(settings), _p(seeds), n, _p(be), _p(bg), _p(ev), _p(cv),
+                                                  _p(nr), recs))
+        out = []
+        for i in range(n):
+            runs = [(recs[i * maxr + k].best_energy, recs[i * maxr + k].iterations,
+                     bool(recs[i * maxr + k].converged)) for k in range(min(int(nr[i]), maxr))]
+            out.append(DockResult(float(be[i]), bg[i], int(ev[i]), bool(cv[i]), runs))
+        return out
+
+
+class DevGrid:
+    """A device-resident receptor map set (mdr_dev_grid), shared by every
+    ligand docked against it."""
+
+    def __init__(self, dev: "Device", handle, grid: Grid):
+        self.dev, self.h, self.grid = dev, handle, grid
+
+    def download(self) -> np.ndarray:
+        g = self.grid
+        maps = np.zeros((g.n_types + 2,) + tuple(int(v) for v in g.shape[::-1]), np.float32)
+        self.dev._chk(self.dev.lib.mdr_grid_download(self.dev.ctx, self.h, _p(maps)))
+        return maps
+
+    def free(self):
+        if self.h:
+            self.dev.lib.mdr_grid_free(self.dev.ctx, self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            if self.dev.ctx:
+                self.free()
+        except Exception:
+            pass
 
 
 @dataclass

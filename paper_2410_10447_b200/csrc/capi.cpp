@@ -58,6 +58,16 @@ struct mdr_dev_instance {
   LigandView view{};
   void* block = nullptr;  // one device allocation holding every array
   int n_atoms = 0, n_sites = 0, n_rot = 0;
+  // grid-map scoring mode (mdr_instance_set_grid)
+  bool grid = false;
+  GridView gview{};
+  FlexView flex{};
+  void* flex_block = nullptr;
+};
+
+struct mdr_dev_grid {
+  GridView view{};
+  float* maps = nullptr;
 };
 
 namespace {
@@ -554,6 +564,7 @@ void mdr_instance_free(mdr_ctx* ctx, mdr_dev_instance* di) {
   if (!di) return;
   if (ctx) cudaStreamSynchronize(ctx->stream);
   cudaFree(di->block);
+  if (di->flex_block) cudaFree(di->flex_block);
   delete di;
 }
 
@@ -562,6 +573,16 @@ struct InstanceGuard {
   mdr_dev_instance* di;
   ~InstanceGuard() { mdr_instance_free(ctx, di); }
 };
+
+// Grid mode runs one CTA of `partition` threads per pose: thread d owns
+// genotype dimension d, so the block must cover the genotype.
+static int check_grid_block(mdr_ctx* ctx, const mdr_dev_instance* di, int partition) {
+  if (partition < 6 + di->n_rot)
+    return fail(ctx, MDR_ERR_BLOCK_SIZE, "grid mode needs partition >= 6 + n_rot (one thread per dimension)");
+  if (grid_smem_for(di->view, di->flex, partition) > 227 * 1024)
+    return fail(ctx, MDR_ERR_SIZE, "grid-mode ligand does not fit in shared memory");
+  return MDR_OK;
+}
 
 // ---------------------------------------------------------------- L2
 static mdr_sync_stats score_stats(int method, int accum, int partition) {
@@ -572,6 +593,13 @@ int mdr_score_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* g, int
                   int partition, float* e, float* grad, float* tq) {
   if (!ctx || !di) return fail(ctx, MDR_ERR_INVALID, "null argument");
   if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (di->grid) {
+    if (int rc = check_grid_block(ctx, di, partition)) return rc;
+    if (n <= 0) return MDR_OK;
+    CK(launch_grid_score(di->view, di->gview, di->flex, g, n, method, partition, e, grad, tq, ctx->stream));
+    ctx->launches++;
+    return MDR_OK;
+  }
   if (n <= 0) return MDR_OK;
   CK(launch_score(di->view, g, n, method, ctx->pair, partition, accum == MDR_ACCUM_HALF, e, grad, tq, ctx->stream,
                   ctx->wpb));
@@ -665,6 +693,14 @@ int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double*
                          int32_t* ocv, int32_t* status) {
   if (!ctx || !di || max_iters < 0) return fail(ctx, MDR_ERR_INVALID, "bad argument");
   if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (di->grid) {
+    if (int rc = check_grid_block(ctx, di, partition)) return rc;
+    if (n <= 0) return MDR_OK;
+    CK(launch_grid_local_search(di->view, di->gview, di->flex, starts, n, max_iters, tol, method, partition, og, oe,
+                                oit, ocv, status, ctx->stream));
+    ctx->launches++;
+    return MDR_OK;
+  }
   if (n <= 0) return MDR_OK;
   CK(launch_local_search(di->view, starts, n, max_iters, tol, method, ctx->pair, partition, accum == MDR_ACCUM_HALF,
                          og, oe, oit, ocv, status, ctx->stream, ctx->wpb, cta_warps_for(ctx)));
@@ -746,6 +782,9 @@ struct mdr_lga_batch {
   int launches = 0;
   int cta_warps = 0;
   mdr_lga_settings settings{};
+  bool grid = false;
+  GridView G{};
+  FlexView F{};
 };
 
 static uint64_t mix64_host(uint64_t z) {
@@ -774,6 +813,7 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
     return nullptr;
   }
   if (check_lga(ctx, method, s)) return nullptr;
+  if (di->grid && check_grid_block(ctx, di, s->partition)) return nullptr;
   mdr_lga_batch* b = new mdr_lga_batch;
   b->L = di->view;
   b->method = method;
@@ -845,9 +885,15 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
     return nullptr;
   }
   b->cta_warps = cta_warps_for(ctx);
-  cudaError_t e = prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
+  b->grid = di->grid;
+  b->G = di->gview;
+  b->F = di->flex;
+  cudaError_t e = b->grid ? prepare_grid_lga(b->L, b->F, method, D.partition)
+                          : prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-  if (e == cudaSuccess) e = launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, b->cta_warps, &b->launches);
+  if (e == cudaSuccess)
+    e = b->grid ? launch_grid_lga(b->L, b->G, b->F, D, method, D.partition, cs, &b->launches)
+                : launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, b->cta_warps, &b->launches);
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(cs, &g);
   if (e == cudaSuccess) e = e2;
@@ -890,7 +936,10 @@ int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaMemcpyAsync(b->seeds, d_seeds, sizeof(uint64_t) * D.R, cudaMemcpyDeviceToDevice, ctx->stream));
   int launches = 0;
-  CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, b->cta_warps, &launches, ev.data()));
+  if (b->grid)
+    CK(launch_grid_lga(b->L, b->G, b->F, D, b->method, D.partition, ctx->stream, &launches, ev.data()));
+  else
+    CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, b->cta_warps, &launches, ev.data()));
   ctx->launches += (uint64_t)launches;
   CK(cudaStreamSynchronize(ctx->stream));
   float tot = 0.f, t = 0.f;
@@ -987,6 +1036,265 @@ int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int ac
   CK(cudaGraphLaunch(b->exec, S(ctx)));
   ctx->launches += (uint64_t)b->launches;
   return mdr_lga_batch_download(ctx, b, best_e, best_g, evals, conv, n_records, records, total);
+}
+
+// ---------------------------------------------------------------- grid mode
+static int check_grid_shape(mdr_ctx* ctx, const mdr_grid* g) {
+  if (!g) return fail(ctx, MDR_ERR_INVALID, "null grid");
+  if (g->nx < 2 || g->ny < 2 || g->nz < 2 || g->n_types < 1 || !(g->spacing > 0.0))
+    return fail(ctx, MDR_ERR_SIZE, "grid needs >= 2 points per axis, >= 1 type map and spacing > 0");
+  if ((long long)g->nx * g->ny * g->nz > (1ll << 31) / (g->n_types + 2))
+    return fail(ctx, MDR_ERR_SIZE, "grid too large");
+  return MDR_OK;
+}
+
+static mdr_dev_grid* grid_alloc(mdr_ctx* ctx, const mdr_grid* g) {
+  mdr_dev_grid* d = new mdr_dev_grid;
+  GridView& v = d->view;
+  v.nx = g->nx;
+  v.ny = g->ny;
+  v.nz = g->nz;
+  v.n_types = g->n_types;
+  v.ox = g->origin[0];
+  v.oy = g->origin[1];
+  v.oz = g->origin[2];
+  v.h = g->spacing;
+  v.inv_h = 1.0 / g->spacing;
+  v.stride = (long long)g->nx * g->ny * g->nz;
+  if (cudaMalloc(&d->maps, sizeof(float) * (size_t)v.stride * (g->n_types + 2)) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "cudaMalloc failed for grid maps");
+    delete d;
+    return nullptr;
+  }
+  v.maps = d->maps;
+  return d;
+}
+
+mdr_dev_grid* mdr_grid_upload(mdr_ctx* ctx, const mdr_grid* g) {
+  if (!ctx || check_grid_shape(ctx, g)) return nullptr;
+  if (!g->maps) {
+    fail(ctx, MDR_ERR_INVALID, "null maps");
+    return nullptr;
+  }
+  mdr_dev_grid* d = grid_alloc(ctx, g);
+  if (!d) return nullptr;
+  const size_t bytes = sizeof(float) * (size_t)d->view.stride * (g->n_types + 2);
+  if (cudaMemcpyAsync(d->maps, g->maps, bytes, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+      cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
+    fail(ctx, MDR_ERR_CUDA, "grid upload failed");
+    mdr_grid_free(ctx, d);
+    return nullptr;
+  }
+  return d;
+}
+
+mdr_dev_grid* mdr_grid_build(mdr_ctx* ctx, const mdr_instance* sites, const mdr_receptor_fields* f,
+                             const mdr_grid* shape) {
+  if (!ctx || check_grid_shape(ctx, shape)) return nullptr;
+  if (!sites || !f || !sites->site_xyzdd || sites->n_sites < 1 || !f->site_charge || !f->site_volume ||
+      !f->type_depth_scale || !f->type_dist_scale || !(f->desolv_sigma > 0.0)) {
+    fail(ctx, MDR_ERR_INVALID, "bad receptor fields");
+    return nullptr;
+  }
+  mdr_dev_grid* d = grid_alloc(ctx, shape);
+  if (!d) return nullptr;
+  const int ns = sites->n_sites, nt = shape->n_types;
+  double* buf = nullptr;
+  const size_t nd = 5 * (size_t)ns + 2 * (size_t)ns + 2 * (size_t)nt;
+  cudaError_t e = cudaMallocAsync(&buf, sizeof(double) * nd, ctx->stream);
+  std::vector<double> h(nd);
+  std::memcpy(h.data(), sites->site_xyzdd, sizeof(double) * 5 * ns);
+  std::memcpy(h.data() + 5 * ns, f->site_charge, sizeof(double) * ns);
+  std::memcpy(h.data() + 6 * ns, f->site_volume, sizeof(double) * ns);
+  std::memcpy(h.data() + 7 * ns, f->type_depth_scale, sizeof(double) * nt);
+  std::memcpy(h.data() + 7 * ns + nt, f->type_dist_scale, sizeof(double) * nt);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(buf, h.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess)
+    e = launch_grid_build(d->view, buf, ns, buf + 5 * ns, buf + 6 * ns, buf + 7 * ns, buf + 7 * ns + nt,
+                          f->elec_scale, f->desolv_sigma, d->maps, ctx->stream);
+  if (e == cudaSuccess) ctx->launches++;
+  if (buf) cudaFreeAsync(buf, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cuda_fail(ctx, e, "mdr_grid_build");
+    mdr_grid_free(ctx, d);
+    return nullptr;
+  }
+  return d;
+}
+
+int mdr_grid_download(mdr_ctx* ctx, const mdr_dev_grid* d, float* maps) {
+  if (!ctx || !d || !maps) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  CK(cudaMemcpyAsync(maps, d->maps, sizeof(float) * (size_t)d->view.stride * (d->view.n_types + 2),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return MDR_OK;
+}
+
+void mdr_grid_free(mdr_ctx* ctx, mdr_dev_grid* d) {
+  if (!d) return;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  cudaFree(d->maps);
+  delete d;
+}
+
+// Host preparation of the grid-mode chemistry (FlexView): per-atom
+// {radius, sqrt(epsilon), q, k_e q} and the torsion-group CSR.
+int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid* g, const mdr_ligand_params* p) {
+  if (!ctx || !di) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (!g) {
+    di->grid = false;
+    return MDR_OK;
+  }
+  if (!p || !p->atom_type || !p->atom_charge || !p->atom_radius || !p->atom_epsilon)
+    return fail(ctx, MDR_ERR_INVALID, "null ligand parameters");
+  const int na = di->n_atoms, nr = di->n_rot;
+  std::vector<int> tors(na), type(na);
+  CK(cudaMemcpy(tors.data(), di->view.tors, sizeof(int) * na, cudaMemcpyDeviceToHost));
+  std::vector<float4> chem(na);
+  for (int i = 0; i < na; ++i) {
+    if (p->atom_type[i] < 0 || p->atom_type[i] >= g->view.n_types)
+      return fail(ctx, MDR_ERR_SIZE, "atom type outside [0, n_types)");
+    if (!(p->atom_epsilon[i] >= 0.0) || !std::isfinite(p->atom_charge[i]) || !std::isfinite(p->atom_radius[i]))
+      return fail(ctx, MDR_ERR_NUMERIC_DOMAIN, "non-finite or negative ligand parameter");
+    type[i] = p->atom_type[i];
+    chem[i] = make_float4((float)p->atom_radius[i], (float)std::sqrt(p->atom_epsilon[i]), (float)p->atom_charge[i],
+                          (float)(p->elec_scale * p->atom_charge[i]));
+  }
+  std::vector<int> off(nr + 1, 0), members;
+  for (int k = 0; k < nr; ++k) {
+    off[k] = (int)members.size();
+    for (int i = 0; i < na; ++i)
+      if (tors[i] == k) members.push_back(i);
+  }
+  off[nr] = (int)members.size();
+  const int nta = (int)members.size();
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t o_type = 0, o_chem = al(sizeof(int) * na), o_off = o_chem + al(sizeof(float4) * na),
+               o_mem = o_off + al(sizeof(int) * (nr + 1)), total = o_mem + al(sizeof(int) * std::max(nta, 1));
+  if (di->flex_block) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(di->flex_block);
+    di->flex_block = nullptr;
+  }
+  CK(cudaMalloc(&di->flex_block, total));
+  char* b = static_cast<char*>(di->flex_block);
+  CK(cudaMemcpy(b + o_type, type.data(), sizeof(int) * na, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_chem, chem.data(), sizeof(float4) * na, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b + o_off, off.data(), sizeof(int) * (nr + 1), cudaMemcpyHostToDevice));
+  if (nta) CK(cudaMemcpy(b + o_mem, members.data(), sizeof(int) * nta, cudaMemcpyHostToDevice));
+  FlexView& F = di->flex;
+  F.type = reinterpret_cast<const int*>(b + o_type);
+  F.chem = reinterpret_cast<const float4*>(b + o_chem);
+  F.grp_off = reinterpret_cast<const int*>(b + o_off);
+  F.grp_atoms = reinterpret_cast<const int*>(b + o_mem);
+  F.n_tors_atoms = nta;
+  F.intra = p->intra != 0;
+  di->gview = g->view;
+  di->grid = true;
+  return MDR_OK;
+}
+
+namespace {
+struct GridLigand {  // a per-call device ligand switched to grid mode
+  mdr_ctx* ctx;
+  mdr_dev_instance* di = nullptr;
+  ~GridLigand() { mdr_instance_free(ctx, di); }
+};
+int grid_ligand(mdr_ctx* ctx, GridLigand& gl, const mdr_dev_grid* g, const mdr_instance* inst,
+                const mdr_ligand_params* p) {
+  if (!g) return fail(ctx, MDR_ERR_INVALID, "null grid");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  gl.di = mdr_instance_upload(ctx, inst);
+  if (!gl.di) return MDR_ERR_CUDA;
+  return mdr_instance_set_grid(ctx, gl.di, g, p);
+}
+}  // namespace
+
+int mdr_grid_score_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instance* inst, const mdr_ligand_params* p,
+                         const double* genos, int n, int method, int partition, float* energy, float* gradient,
+                         float* torque) {
+  if (!ctx || n < 0 || (n && (!genos || !energy || !gradient || !torque)))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  GridLigand gl{ctx};
+  if (int rc = grid_ligand(ctx, gl, g, inst, p)) return rc;
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (int rc = check_grid_block(ctx, gl.di, partition)) return rc;
+  if (n == 0) return MDR_OK;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> dg;
+  DevBuf<float> de, dgr, dt;
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dgr.alloc((size_t)n * dim, S(ctx)));
+  CK(dt.alloc((size_t)n * 3, S(ctx)));
+  CK(cudaMemcpyAsync(dg.p, genos, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  if (int rc = mdr_score_dev(ctx, gl.di, dg.p, n, method, MDR_ACCUM_SINGLE, partition, de.p, dgr.p, dt.p)) return rc;
+  CK(cudaMemcpyAsync(energy, de.p, sizeof(float) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(gradient, dgr.p, sizeof(float) * n * dim, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(torque, dt.p, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_grid_local_search_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instance* inst,
+                                const mdr_ligand_params* p, const double* starts, int n, int max_iters, double tol,
+                                int method, int partition, double* out_g, double* out_e, int32_t* out_it,
+                                int32_t* out_cv) {
+  if (!ctx || n < 0 || max_iters < 0 || (n && (!starts || !out_g || !out_e || !out_it || !out_cv)))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  GridLigand gl{ctx};
+  if (int rc = grid_ligand(ctx, gl, g, inst, p)) return rc;
+  if (int rc = check_partition(ctx, partition, method)) return rc;
+  if (int rc = check_grid_block(ctx, gl.di, partition)) return rc;
+  if (n == 0) return MDR_OK;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> ds, dg, de;
+  DevBuf<int> dit, dcv, dst;
+  CK(ds.alloc((size_t)n * dim, S(ctx)));
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dit.alloc(n, S(ctx)));
+  CK(dcv.alloc(n, S(ctx)));
+  CK(dst.alloc(n, S(ctx)));
+  CK(cudaMemsetAsync(dst.p, 0, sizeof(int) * n, S(ctx)));
+  CK(cudaMemcpyAsync(ds.p, starts, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  if (int rc = mdr_local_search_dev(ctx, gl.di, ds.p, n, max_iters, tol, method, MDR_ACCUM_SINGLE, partition, dg.p,
+                                    de.p, dit.p, dcv.p, dst.p))
+    return rc;
+  std::vector<int> status(n);
+  CK(cudaMemcpyAsync(out_g, dg.p, sizeof(double) * n * dim, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_e, de.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_it, dit.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(out_cv, dcv.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(status.data(), dst.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  for (int i = 0; i < n; ++i)
+    if (status[i] != MDR_OK) return fail(ctx, status[i], "adadelta_step: non-finite gradient component");
+  return MDR_OK;
+}
+
+int mdr_grid_lga_run_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instance* inst,
+                           const mdr_ligand_params* p, int method, const mdr_lga_settings* s, const uint64_t* seeds,
+                           int n_runs, double* best_e, double* best_g, int64_t* evals, int32_t* conv,
+                           int32_t* n_records, mdr_ls_record* records) {
+  if (!ctx || n_runs < 0 || (n_runs && !seeds)) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  GridLigand gl{ctx};
+  if (int rc = grid_ligand(ctx, gl, g, inst, p)) return rc;
+  if (int rc = check_lga(ctx, method, s)) return rc;
+  if (n_runs == 0) return MDR_OK;
+  mdr_lga_batch* b = mdr_lga_batch_create(ctx, gl.di, method, MDR_ACCUM_SINGLE, s, n_runs);
+  if (!b) return MDR_ERR_CUDA;
+  int rc = MDR_OK;
+  if (cudaMemcpyAsync(b->seeds, seeds, sizeof(uint64_t) * n_runs, cudaMemcpyHostToDevice, S(ctx)) != cudaSuccess ||
+      cudaGraphLaunch(b->exec, S(ctx)) != cudaSuccess)
+    rc = fail(ctx, MDR_ERR_CUDA, "grid LGA launch failed");
+  if (rc == MDR_OK) {
+    ctx->launches += (uint64_t)b->launches;
+    rc = mdr_lga_batch_download(ctx, b, best_e, best_g, evals, conv, n_records, records, nullptr);
+  }
+  mdr_lga_batch_destroy(ctx, b);
+  return rc;
 }
 
 }  // extern "C"

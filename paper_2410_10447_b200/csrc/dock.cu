@@ -12,6 +12,7 @@
 
 #include "dock_launch.h"
 #include "mdr_device.cuh"
+#include "lga_device.cuh"
 
 namespace mdr {
 
@@ -115,17 +116,6 @@ __global__ void scoreref_kernel(LigandView L, const double* __restrict__ genos, 
 }
 
 // ---------------------------------------------------------- ADADELTA
-// adadelta_step docking.cpp:297-305 for the lane-owned dimension d.
-__device__ __forceinline__ void adadelta_dim(double& sq_g, double& sq_u, double& x, double gd, int d, double rho,
-                                             double eps) {
-  const double old_u = sq_u;
-  sq_g = rho * sq_g + (1.0 - rho) * gd * gd;
-  const double delta = -sqrt(old_u + eps) / sqrt(sq_g + eps) * gd;
-  sq_u = rho * old_u + (1.0 - rho) * delta * delta;
-  x = x + delta;
-  if (d >= 3) x = wrap_angle(x);  // normalize_angles docking.cpp:172-179
-}
-
 __global__ void adadelta_kernel(int dim, int n, double rho, double eps, double* sq_g, double* sq_u, double* geno,
                                 const double* grad, int* status) {
   const int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -415,10 +405,6 @@ __global__ void ls_cta_kernel(LigandView L, const double* __restrict__ starts, i
 }
 
 // ------------------------------------------------------------- K5 LGA
-__device__ __forceinline__ uint64_t run_key(const LgaDev& D, int run) {
-  return mix64(D.seeds[run] ^ D.label_hash);  // RngStream ctor rng.cpp:31-32
-}
-
 // lga init: random_genotype docking.cpp:360-388 + score, warp per individual.
 template <int METHOD, int PAIR>
 __global__ void lga_init_kernel(LigandView L, LgaDev D) {
@@ -445,18 +431,6 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
   Frame f;
   const ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
   if (lane == 0) D.pope[0][(size_t)run * D.P + p] = (double)o.sums[0];
-}
-
-__device__ __forceinline__ void track_best(const LgaDev& D, int run, const double* g, double e) {
-  if (e < D.best_e[run]) {  // strict: first occurrence wins (docking.cpp:408-413)
-    D.best_e[run] = e;
-    for (int d = 0; d < D.dim; ++d) D.best_g[(size_t)run * D.dim + d] = g[d];
-  }
-}
-
-__device__ __forceinline__ bool budget_ok(const LgaDev& D, long long evals) {
-  // docking.cpp:430-435
-  return evals + D.off + (long long)D.L * (D.ls_iters + 1) <= D.max_evals;
 }
 
 __global__ void lga_init_finalize(LgaDev D) {
@@ -527,26 +501,6 @@ __global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
   if (lane == 0) ne[1 + i] = (double)o.sums[0];
 }
 
-// Index (1..off) of the offspring of rank r in the stable (energy, index)
-// order of docking.cpp:476-483; every lane of the calling warp gets it.
-__device__ __forceinline__ int ls_target(const LgaDev& D, int run, int r) {
-  const int lane = threadIdx.x & 31;
-  const double* ne = D.pope[D.cur[run] ^ 1] + (size_t)run * D.P;
-  int target = -1;
-  for (int j = 1 + lane; j <= D.off; j += 32) {
-    const double ej = ne[j];
-    int rank = 0;
-    for (int k = 1; k <= D.off; ++k) {
-      const double ek = ne[k];
-      rank += (ek < ej) || (ek == ej && k < j);
-    }
-    if (rank == r) target = j;
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) target = max(target, __shfl_xor_sync(kFull, target, off));
-  return target;
-}
-
 // Fast pair modes: one CTA per local search (CTA-per-pose kernel K4c).
 template <int METHOD, int PAIR>
 __global__ void lga_ls_cta_kernel(LigandView L, LgaDev D) {
@@ -603,18 +557,6 @@ __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
     D.lstarget[o] = target;
     if (res.status != MDR_OK) D.status[run] = res.status;
   }
-}
-
-__device__ __forceinline__ void push_record(const LgaDev& D, int run, double e, int it, int cv) {
-  const int k = D.nrec[run];
-  if (k < D.maxrec) {
-    mdr_ls_record rec;
-    rec.best_energy = e;
-    rec.iterations = it;
-    rec.converged = cv;
-    D.recs[(size_t)run * D.maxrec + k] = rec;
-  }
-  D.nrec[run] = k + 1;
 }
 
 // Sequential bookkeeping of one generation, in the reference's order:
@@ -869,6 +811,16 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;
   if (n_launches) *n_launches = launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lga_init_finalize(const LgaDev& D, cudaStream_t s) {
+  lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lga_gen_finalize(const LgaDev& D, int gen, cudaStream_t s) {
+  lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,22 @@ cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int 
 cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pair, cudaStream_t s, int wpb,
                        int cta_warps, int* n_launches, cudaEvent_t* ls_events = nullptr);
 cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s);
+cudaError_t launch_lga_init_finalize(const LgaDev& D, cudaStream_t s);
+cudaError_t launch_lga_gen_finalize(const LgaDev& D, int gen, cudaStream_t s);
+
+// grid.cu (grid-map scoring mode, CTA of `threads` per pose)
+size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads);
+cudaError_t launch_grid_score(const LigandView& L, const GridView& G, const FlexView& F, const double* genos, int n,
+                              int method, int threads, float* energy, float* grad, float* torque, cudaStream_t s);
+cudaError_t launch_grid_local_search(const LigandView& L, const GridView& G, const FlexView& F, const double* starts,
+                                     int n, int max_iters, double tol, int method, int threads, double* out_g,
+                                     double* out_e, int* out_it, int* out_cv, int* status, cudaStream_t s);
+cudaError_t prepare_grid_lga(const LigandView& L, const FlexView& F, int method, int threads);
+cudaError_t launch_grid_lga(const LigandView& L, const GridView& G, const FlexView& F, const LgaDev& D, int method,
+                            int threads, cudaStream_t s, int* n_launches, cudaEvent_t* ls_events = nullptr);
+cudaError_t launch_grid_build(const GridView& G, const double* sites, int n_sites, const double* charge,
+                              const double* volume, const double* depth_scale, const double* dist_scale,
+                              double elec_scale, double sigma, float* maps, cudaStream_t s);
 
 // reduce.cu
 cudaError_t launch_f32_to_half(const float* in, size_t n, uint16_t* out, cudaStream_t s);

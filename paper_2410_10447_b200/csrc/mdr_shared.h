@@ -36,6 +36,27 @@ struct LigandView {
   const double* box;        // device: lo[3], hi[3] random_genotype bounds incl. margin
 };
 
+// Grid-map scoring mode (mdr.h).  Maps are FP32,
+// [(n_types + 2)][nz][ny][nx] (type maps, electrostatic, desolvation).
+struct GridView {
+  int nx, ny, nz, n_types;
+  double ox, oy, oz, h, inv_h;
+  long long stride;  // nx * ny * nz
+  const float* maps;
+};
+
+// Ligand chemistry of grid mode, prepared on the host (capi.cpp):
+//   chem[i] = {radius_i, sqrt(epsilon_i), charge_i, elec_scale * charge_i};
+//   grp_atoms: the torsioned atoms grouped by torsion (ascending k, then
+//   ascending atom index), grp_off[k] .. grp_off[k + 1] delimiting group k.
+struct FlexView {
+  const int* type;
+  const float4* chem;
+  const int* grp_off;    // n_rot + 1
+  const int* grp_atoms;  // n_tors_atoms
+  int n_tors_atoms, intra;
+};
+
 // All device state of a batch of LGA runs (docking.cpp:392-517).
 struct LgaDev {
   int R, P, dim, off, L, gens, ls_iters, maxrec, partition, half_mode;
