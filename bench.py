@@ -479,9 +479,83 @@ def mode_sweep(lib, torch, local, inst, settings, steps=3):
     return out
 
 
+def grid_flop_bytes_per_eval(inst, params, partition):
+    """Algorithmic work of one grid-mode evaluation:
+    bytes = atoms x 8 corners x 3 maps x 4 B (the gathered map values);
+    flops = 30 per intramolecular pair (soft-core 12-6 + Coulomb + force) +
+            ~80 per atom (placement 30, combine 24, trilinear 21, torque 6)."""
+    tors = inst.torsion
+    pairs = sum(1 for i in range(inst.n_atoms) for j in range(i + 1, inst.n_atoms) if tors[i] != tors[j])
+    return 80 * inst.n_atoms + (30 * pairs if params.intra else 0), 96 * inst.n_atoms, pairs
+
+
+def c4_measure(lib, torch, local, methods=("baseline", "split", "tcu"), partitions=(128,), steps=3, runs=N_RUNS):
+    """C4 (BASELINE.json configs[3]) on this GPU: 100-atom / 30-torsion
+    ligand, grid mode on 126^3 maps, `runs` LGA runs, device resident, events
+    on the launching stream, L2 flushed before every step."""
+    from paper_2410_10447_b200 import Device
+    from paper_2410_10447_b200.workloads import c4
+
+    inst, params, fields, grid, settings = c4()
+    stream = torch.cuda.current_stream()
+    seeds = torch.from_numpy((np.arange(runs, dtype=np.uint64) + np.uint64(2_000_000)).view(np.int64)).to(
+        f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    dev = Device(local)
+    dev.set_stream(stream.cuda_stream)
+    dg = lib.mdr_grid_build(dev.ctx, inst.cref(), fields.cref(), grid.cref())
+    assert dg, lib.mdr_last_error(dev.ctx)
+    di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+    assert lib.mdr_instance_set_grid(dev.ctx, di, dg, params.cref()) == 0, lib.mdr_last_error(dev.ctx)
+    flop, nbytes, pairs = grid_flop_bytes_per_eval(inst, params, 128)
+    out = {"workload": "C4 large flexible ligand: 100 atoms / 30 torsions, grid mode (126^3 x 6 maps, 0.375 A, "
+                       f"intramolecular on, {pairs} pairs), {runs} LGA runs (BASELINE.json configs[3])",
+           "map_bytes": int(grid.n_points * (grid.n_types + 2) * 4), "flop_per_eval": flop,
+           "map_bytes_per_eval": nbytes, "l2": "flushed (256 MB write) before every step", "results": {}}
+    for part in partitions:
+        for mname in methods:
+            s = LgaSettings(partition=part)
+            b = lib.mdr_lga_batch_create(dev.ctx, di, METHODS[mname], SINGLE, C.byref(s), runs)
+            assert b, lib.mdr_last_error(dev.ctx)
+            tot = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+            for _ in range(2):
+                lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+            lib.mdr_lga_batch_total_evals_dev(dev.ctx, b, C.c_void_p(tot.data_ptr()))
+            torch.cuda.synchronize()
+            ev = int(tot.item())
+            ms = []
+            for k in range(steps):
+                flush.fill_(float(k))
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+                e.record(stream)
+                e.synchronize()
+                ms.append(a.elapsed_time(e))
+            ls_ms, all_ms, ls_ev = C.c_float(), C.c_float(), C.c_int64()
+            lib.mdr_lga_batch_profile_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()), C.byref(ls_ms), C.byref(all_ms),
+                                          C.byref(ls_ev))
+            t = statistics.median(ms)
+            ls_s = ls_ms.value * 1e-3
+            out["results"][f"{mname}/p{part}"] = {
+                "evals_per_s": ev / (t * 1e-3), "ms_per_step": t, "evals_per_step": ev,
+                "docking_sec_per_ligand": t * 1e-3,
+                "ls_kernel_share": ls_ms.value / all_ms.value if all_ms.value else None,
+                "ls_kernel_ms_per_launch": ls_ms.value / (s.generations + 1),
+                "ls_map_GBps": nbytes * ls_ev.value / ls_s / 1e9 if ls_s else None,
+                "ls_TFLOPs": flop * ls_ev.value / ls_s / 1e12 if ls_s else None}
+            lib.mdr_lga_batch_destroy(dev.ctx, b)
+    lib.mdr_instance_free(dev.ctx, di)
+    lib.mdr_grid_free(dev.ctx, dg)
+    dev.close()
+    return out
+
+
 def extra_measurements(args, dev, lib, torch):
-    """Mode sweep of the docking step + C2 reduction microbench (ns/call)."""
+    """Mode sweep of the docking step, C4 grid-mode docking, C2 reduction
+    microbench (ns/call)."""
     out = {"modes": mode_sweep(lib, torch, torch.cuda.current_device(), workload(), LgaSettings())}
+    out["c4_grid"] = c4_measure(lib, torch, torch.cuda.current_device())
     if hasattr(lib, "mdr_reduce_bench_dev"):
         from paper_2410_10447_b200.microbench import reduce_microbench
 
