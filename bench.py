@@ -551,11 +551,45 @@ def c4_measure(lib, torch, local, methods=("baseline", "split", "tcu"), partitio
     return out
 
 
+def c5_measure(torch, local, n_ligands=256, runs=10, method="baseline", batch=256):
+    """C5 (BASELINE.json configs[4]) sample on this GPU: `n_ligands` synthetic
+    ligands (U[10,100] atoms, U[0,30] torsions) against the C4 receptor
+    (126^3 maps), `runs` LGA runs each, docked + clustered through the
+    screening driver (mdr_grid_screen_batch: host ligands in, results out,
+    so this is an end-to-end figure).  Reports ligands/hour."""
+    from paper_2410_10447_b200 import Device
+    from paper_2410_10447_b200 import screen as sc
+    from paper_2410_10447_b200.workloads import c4_receptor, c5_ligand
+
+    sites, fields, grid = c4_receptor()
+    dev = Device(local)
+    dev.set_stream(torch.cuda.current_stream().cuda_stream)
+    dg = dev.grid_build(sites, fields, grid)
+    s = LgaSettings(partition=64)
+    ligs = [c5_ligand(j, sites) for j in range(n_ligands)]
+    warm = sc.screen(dev, dg, lambda j: ligs[j], 8, 2, LgaSettings(partition=64, generations=2), METHODS[method])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rows, clusters = sc.screen(dev, dg, lambda j: ligs[j], n_ligands, runs, s, METHODS[method], batch=batch)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    evals = sum(r.evaluations for r in rows)
+    out = {"workload": f"C5 virtual-screen sample: {n_ligands} ligands (U[10,100] atoms, U[0,30] torsions) x {runs} "
+                       "LGA runs vs the C4 receptor (126^3 maps), grid mode, per-ligand RMSD clustering (2 A)",
+           "ligands_per_hour": sc.ligands_per_hour(n_ligands, dt), "seconds": dt, "evals_per_s": evals / dt,
+           "evaluations": evals, "mean_clusters": float(np.mean([c[1] for c in clusters.values()])),
+           "api": "screen.screen -> mdr_grid_screen_batch (host ligands in, CSV rows out)", "warmup": len(warm[0])}
+    dg.free()
+    dev.close()
+    return out
+
+
 def extra_measurements(args, dev, lib, torch):
     """Mode sweep of the docking step, C4 grid-mode docking, C2 reduction
     microbench (ns/call)."""
     out = {"modes": mode_sweep(lib, torch, torch.cuda.current_device(), workload(), LgaSettings())}
     out["c4_grid"] = c4_measure(lib, torch, torch.cuda.current_device())
+    out["c5_screen"] = c5_measure(torch, torch.cuda.current_device())
     if hasattr(lib, "mdr_reduce_bench_dev"):
         from paper_2410_10447_b200.microbench import reduce_microbench
 

@@ -340,6 +340,46 @@ int mdr_grid_lga_run_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_ins
                            int64_t* evaluations, int32_t* converged, int32_t* n_records,
                            mdr_ls_record* records);
 
+/* ---- virtual screen (BASELINE config C5) -------------------
+ * Dock n_ligands ligands against one device receptor in ONE launch sequence:
+ * runs_per_ligand LGA runs each (run r = j * runs_per_ligand + k docks
+ * ligand j with seeds[r]), grid-mode scoring, then the RMSD clustering of
+ * each ligand's best poses.  Every run is exactly the run a single-ligand
+ * mdr_grid_lga_run_batch would make (same kernels, same draws).  All ligands
+ * share settings->partition threads per pose (>= 6 + n_rot of each).
+ * Outputs per run: best_energy, evaluations, converged, cluster_of,
+ * rmsd_to_seed (each n_ligands * runs_per_ligand); best_genotype packed per
+ * ligand (ligand j's runs * (6 + n_rot_j) doubles follow ligand j-1's);
+ * n_clusters per ligand.  Null output pointers are skipped. */
+int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_instance* ligands,
+                          const mdr_ligand_params* params, int n_ligands, int runs_per_ligand, int method,
+                          const mdr_lga_settings* settings, const uint64_t* seeds, double rmsd_tol,
+                          double* best_energy, double* best_genotype, int64_t* evaluations, int32_t* converged,
+                          int32_t* cluster_of, double* rmsd_to_seed, int32_t* n_clusters);
+
+/* ---- RMSD clustering of docked poses ----------------------
+ * Not in the reference.  Poses become world coordinates through
+ * evaluate_atoms' transform (docking.cpp:101-106, FP64); clustering is
+ * AutoDock's: poses in ascending (energy, index) order, each joins the first
+ * cluster whose seed (lowest-energy member) is within RMSD < rmsd_tol, else
+ * seeds a new cluster.  cluster_of[i] = cluster index in creation order
+ * (0 = the cluster of the best pose); rmsd_to_seed[i] = RMSD to that seed.
+ * CPU restatement: orc_cluster_poses (oracle/mdr_oracle.c). */
+/* genotypes n x dim -> xyz n x n_atoms x 3 (world coordinates). */
+int mdr_pose_coords_batch(mdr_ctx* ctx, const mdr_instance* inst, const double* genotypes, int n, double* xyz);
+int mdr_cluster_poses(mdr_ctx* ctx, const mdr_instance* inst, const double* genotypes, const double* energies,
+                      int n, double rmsd_tol, int32_t* cluster_of, double* rmsd_to_seed, int32_t* n_clusters);
+/* Device variant over segments (one independent clustering per segment,
+ * e.g. per ligand of a screen): poses d_seg_off[s] .. d_seg_off[s+1]. */
+int mdr_cluster_segments_dev(mdr_ctx* ctx, const mdr_dev_instance* dinst, const double* d_genotypes,
+                             const double* d_energies, const int32_t* d_seg_off, int n_seg, int n_total,
+                             double rmsd_tol, int32_t* d_cluster_of, double* d_rmsd_to_seed,
+                             int32_t* d_n_clusters);
+/* Cluster the best poses of an LGA batch's runs (on the device; results to
+ * host buffers of n_runs entries). */
+int mdr_lga_batch_cluster(mdr_ctx* ctx, mdr_lga_batch* b, double rmsd_tol, int32_t* cluster_of,
+                          double* rmsd_to_seed, int32_t* n_clusters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -979,3 +979,88 @@ int orc_grid_lga_run(const mdr_instance* in, const mdr_grid* G, const mdr_ligand
   return lga_core(grid_score_fn, &c, in, s, seed, best_e, best_g, evals_out, conv, n_records, records,
                   max_records);
 }
+
+/* ======================================================== RMSD clustering
+ * SURVEY §8 f3 (north_star: "final best-pose energies and RMSD clustering
+ * must match"); not in the reference.  Pose -> atom coordinates is
+ * evaluate_atoms' transform (docking.cpp:101-106, FP64, reference order);
+ * clustering is AutoDock's: poses in ascending (energy, index) order, each
+ * joins the first existing cluster whose seed (its lowest-energy member) is
+ * within rmsd < tol, else it seeds a new cluster.  RMSD is over atoms in
+ * index correspondence, sqrt(sum |x_i - y_i|^2 / n_atoms). */
+int orc_pose_coords(const mdr_instance* in, const double* g, double* xyz) {
+  if (in->n_rot > 58) return MDR_ERR_SIZE;
+  frame_t f;
+  v3 tw[64];
+  f.tors_world = tw;
+  build_frame(in, g, &f);
+  const v3 t = {{g[0], g[1], g[2]}};
+  for (int i = 0; i < in->n_atoms; ++i) {
+    const double* at = in->atom_xyzw + 4 * i;
+    v3 local = {{at[0], at[1], at[2]}};
+    const int k = in->atom_torsion[i];
+    if (k >= 0) {
+      const v3 ax = orc_torsion_axis(k);
+      const double ang = g[6 + k], c = cos(ang), s = sin(ang);
+      local = add3(add3(scl3(c, local), scl3(s, cross3(ax, local))), scl3((1.0 - c) * dot3(ax, local), ax));
+    }
+    const v3 w = add3(t, mv3(&f.R, local));
+    xyz[3 * i] = w.v[0];
+    xyz[3 * i + 1] = w.v[1];
+    xyz[3 * i + 2] = w.v[2];
+  }
+  return MDR_OK;
+}
+
+static double rmsd_xyz(const double* a, const double* b, int na) {
+  double s = 0.0;
+  for (int i = 0; i < 3 * na; ++i) {
+    const double d = a[i] - b[i];
+    s += d * d;
+  }
+  return sqrt(s / na);
+}
+
+int orc_cluster_poses(const mdr_instance* in, const double* genos, const double* energy, int n, double tol,
+                      int32_t* cluster_of, double* rmsd_to_seed, int32_t* n_clusters) {
+  const int dim = 6 + in->n_rot, na = in->n_atoms;
+  double* xyz = (double*)malloc(sizeof(double) * 3 * (size_t)na * (size_t)(n > 0 ? n : 1));
+  int* order = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+  int* seeds = (int*)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+  int rc = MDR_OK;
+  for (int i = 0; i < n && rc == MDR_OK; ++i) rc = orc_pose_coords(in, genos + (size_t)i * dim, xyz + (size_t)3 * na * i);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  for (int i = 1; i < n; ++i) { /* stable insertion sort by energy */
+    const int v = order[i];
+    int j = i - 1;
+    while (j >= 0 && energy[order[j]] > energy[v]) {
+      order[j + 1] = order[j];
+      --j;
+    }
+    order[j + 1] = v;
+  }
+  int nc = 0;
+  for (int q = 0; q < n && rc == MDR_OK; ++q) {
+    const int p = order[q];
+    int c = -1;
+    double r = 0.0;
+    for (int k = 0; k < nc; ++k) {
+      const double d = rmsd_xyz(xyz + (size_t)3 * na * p, xyz + (size_t)3 * na * seeds[k], na);
+      if (d < tol) {
+        c = k;
+        r = d;
+        break;
+      }
+    }
+    if (c < 0) {
+      c = nc;
+      seeds[nc++] = p;
+      r = 0.0;
+    }
+    cluster_of[p] = c;
+    if (rmsd_to_seed) rmsd_to_seed[p] = r;
+  }
+  *n_clusters = nc;
+  free(xyz); free(order); free(seeds);
+  return rc;
+}

@@ -266,3 +266,23 @@ class Oracle:
                 for i in range(min(nr.value, maxr))]
         return dict(best_energy=be.value, best_genotype=g, evaluations=ev.value, converged=bool(cv.value),
                     runs=runs)
+
+    # ---- RMSD clustering (port only) ---------------------------------------
+    def pose_coords(self, inst, g):
+        g = np.ascontiguousarray(g, np.float64)
+        xyz = np.zeros((inst.n_atoms, 3))
+        self._chk(self.lib.orc_pose_coords(inst.cref(), dptr(g), dptr(xyz)))
+        return xyz
+
+    def cluster_poses(self, inst, genotypes, energies, rmsd_tol=2.0):
+        f = self.lib.orc_cluster_poses
+        f.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int, C.c_double,
+                      C.c_void_p, C.POINTER(C.c_double), C.c_void_p]
+        g = np.ascontiguousarray(genotypes, np.float64).reshape(-1, inst.dim)
+        e = np.ascontiguousarray(energies, np.float64).reshape(-1)
+        n = g.shape[0]
+        c = np.zeros(n, np.int32)
+        r = np.zeros(n)
+        nc = C.c_int32()
+        self._chk(f(inst.cref(), dptr(g), dptr(e), n, rmsd_tol, c.ctypes.data, dptr(r), C.byref(nc)))
+        return c, r, nc.value

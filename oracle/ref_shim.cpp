@@ -337,4 +337,32 @@ int ref_parse_instance(const char* text, int cap_atoms, int cap_sites, int32_t* 
     }
 }
 
+// write_results instance_io.cpp:277-287 over n rows given as parallel
+// arrays; the CSV text (NUL-terminated, truncated to cap) goes to out.
+int ref_write_results(int n, const uint64_t* seed, const char* const* method, const char* const* accum,
+                      const char* const* instance, const double* best_energy, const int64_t* evaluations,
+                      const int32_t* converged, const uint64_t* block_syncs, const uint64_t* atomic_adds,
+                      const uint64_t* mma_ops, char* out, size_t cap, size_t* len) {
+    return guarded([&] {
+        std::vector<ResultRow> rows(n);
+        for (int i = 0; i < n; ++i) {
+            rows[i].seed = seed[i];
+            rows[i].method = method[i];
+            rows[i].accum_mode = accum[i];
+            rows[i].instance = instance[i];
+            rows[i].best_energy = best_energy[i];
+            rows[i].evaluations = evaluations[i];
+            rows[i].converged = converged[i] != 0;
+            rows[i].block_syncs = block_syncs[i];
+            rows[i].atomic_adds = atomic_adds[i];
+            rows[i].mma_ops = mma_ops[i];
+        }
+        const std::string s = write_results(rows);
+        *len = s.size();
+        const size_t k = s.size() < cap ? s.size() : cap - 1;
+        std::memcpy(out, s.data(), k);
+        out[k] = 0;
+    });
+}
+
 } // extern "C"

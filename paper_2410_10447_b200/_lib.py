@@ -69,6 +69,11 @@ _SIGS = {
     "mdr_grid_score_batch": (I, [P, P, P, P, P, I, I, I, P, P, P]),
     "mdr_grid_local_search_batch": (I, [P, P, P, P, P, I, I, D, I, I, P, P, P, P]),
     "mdr_grid_lga_run_batch": (I, [P, P, P, P, I, P, P, I, P, P, P, P, P, P]),
+    "mdr_pose_coords_batch": (I, [P, P, P, I, P]),
+    "mdr_grid_screen_batch": (I, [P, P, P, P, I, I, I, P, P, D, P, P, P, P, P, P, P]),
+    "mdr_cluster_poses": (I, [P, P, P, P, I, D, P, P, P]),
+    "mdr_cluster_segments_dev": (I, [P, P, P, P, P, I, I, D, P, P, P]),
+    "mdr_lga_batch_cluster": (I, [P, P, D, P, P, P]),
 }
 
 # Optional entry points (present once their module is built).

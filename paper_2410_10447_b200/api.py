@@ -290,6 +290,25 @@ class Device:
     def lga_run(self, inst, method, accum, settings: LgaSettings, seed: int) -> DockResult:
         return self.lga_run_batch(inst, method, accum, settings, [seed])[0]
 
+    # ------------------------------------------------- clustering (§8 f3)
+    def pose_coords(self, inst: Instance, genotypes) -> np.ndarray:
+        """World coordinates of poses (evaluate_atoms' transform, docking.cpp:101-106)."""
+        g = np.ascontiguousarray(genotypes, np.float64).reshape(-1, inst.dim)
+        xyz = np.zeros((g.shape[0], inst.n_atoms, 3))
+        self._chk(self.lib.mdr_pose_coords_batch(self.ctx, inst.cref(), _p(g), g.shape[0], _p(xyz)))
+        return xyz
+
+    def cluster_poses(self, inst: Instance, genotypes, energies, rmsd_tol: float = 2.0):
+        """AutoDock clustering of poses: (cluster_of, rmsd_to_seed, n_clusters)."""
+        g = np.ascontiguousarray(genotypes, np.float64).reshape(-1, inst.dim)
+        e = np.ascontiguousarray(energies, np.float64).reshape(-1)
+        n = g.shape[0]
+        c = np.zeros(n, np.int32)
+        r = np.zeros(n)
+        nc = np.zeros(1, np.int32)
+        self._chk(self.lib.mdr_cluster_poses(self.ctx, inst.cref(), _p(g), _p(e), n, rmsd_tol, _p(c), _p(r), _p(nc)))
+        return c, r, int(nc[0])
+
     # ------------------------------------------------- grid-map mode (§8 f1)
     # include/mdr.h "grid-map scoring mode": partition = CTA threads per pose
     # (>= 6 + n_rot); accum does not apply (fp32 / tf32 reductions).
@@ -328,6 +347,42 @@ class Device:
                                                        max_iters, tol, method, partition, _p(g), _p(e), _p(it),
                                                        _p(cv)))
         return [LocalSearchResult(g[i], float(e[i]), int(it[i]), bool(cv[i]), SyncStats()) for i in range(n)]
+
+    def grid_screen_batch(self, dgrid: DevGrid, ligands, params, runs_per_ligand: int, method,
+                          settings: LgaSettings, seeds, rmsd_tol: float = 2.0):
+        """Virtual-screen batch (mdr_grid_screen_batch): every ligand docked
+        runs_per_ligand times in one launch sequence, then clustered.
+        Returns one dict per ligand: best_energy[runs], best_genotype[runs,dim],
+        evaluations[runs], converged[runs], cluster_of[runs], rmsd_to_seed[runs],
+        n_clusters."""
+        from ._abi import CInstance, CLigandParams
+
+        n = len(ligands)
+        R = n * runs_per_ligand
+        seeds = np.ascontiguousarray(seeds, np.uint64).reshape(-1)
+        if seeds.size != R:
+            raise ValueError("need one seed per (ligand, run)")
+        ci = (CInstance * n)(*[l.c() for l in ligands])
+        cp = (CLigandParams * n)(*[p.c() for p in params])
+        be = np.zeros(R)
+        bg = np.zeros(sum(runs_per_ligand * l.dim for l in ligands))
+        ev = np.zeros(R, np.int64)
+        cv = np.zeros(R, np.int32)
+        cl = np.zeros(R, np.int32)
+        rm = np.zeros(R)
+        nc = np.zeros(n, np.int32)
+        self._chk(self.lib.mdr_grid_screen_batch(self.ctx, dgrid.h, ci, cp, n, runs_per_ligand, method,
+                                                 C.byref(settings), _p(seeds), rmsd_tol, _p(be), _p(bg), _p(ev),
+                                                 _p(cv), _p(cl), _p(rm), _p(nc)))
+        out, o = [], 0
+        for j, l in enumerate(ligands):
+            sl = slice(j * runs_per_ligand, (j + 1) * runs_per_ligand)
+            k = runs_per_ligand * l.dim
+            out.append(dict(best_energy=be[sl].copy(), best_genotype=bg[o:o + k].reshape(runs_per_ligand, l.dim),
+                            evaluations=ev[sl].copy(), converged=cv[sl].astype(bool), cluster_of=cl[sl].copy(),
+                            rmsd_to_seed=rm[sl].copy(), n_clusters=int(nc[j])))
+            o += k
+        return out
 
     def grid_lga_run_batch(self, dgrid: DevGrid, inst: Instance, params: LigandParams, method,
                            settings: LgaSettings, seeds):

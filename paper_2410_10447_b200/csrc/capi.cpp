@@ -454,6 +454,28 @@ static int check_instance(mdr_ctx* ctx, const mdr_instance* in) {
   return MDR_OK;
 }
 
+// random_genotype's box (docking.cpp:362-374): site bounding box +- (max d0 + 1).
+static void genotype_box(const mdr_instance* in, double box[6]) {
+  double lo[3] = {std::numeric_limits<double>::max(), std::numeric_limits<double>::max(),
+                  std::numeric_limits<double>::max()};
+  double hi[3] = {std::numeric_limits<double>::lowest(), std::numeric_limits<double>::lowest(),
+                  std::numeric_limits<double>::lowest()};
+  double max_d0 = 0.0;
+  for (int j = 0; j < in->n_sites; ++j) {
+    const double* s = in->site_xyzdd + 5 * j;
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], s[a]);
+      hi[a] = std::max(hi[a], s[a]);
+    }
+    max_d0 = std::max(max_d0, s[4]);
+  }
+  const double margin = max_d0 + 1.0;
+  for (int a = 0; a < 3; ++a) {
+    box[a] = lo[a] - margin;
+    box[3 + a] = hi[a] + margin;
+  }
+}
+
 // Device layout of one ligand: a single allocation
 //   sites | atoms | torsion axes | torsion ids | fp32 sites | fp32 consts | box
 namespace {
@@ -784,7 +806,9 @@ struct mdr_lga_batch {
   mdr_lga_settings settings{};
   bool grid = false;
   GridView G{};
-  FlexView F{};
+  GridLigands GL{};    // device tables (one ligand, or a screen batch)
+  void* gl_block = nullptr;
+  size_t gsm = 0;      // dynamic shared memory of the grid kernels
 };
 
 static uint64_t mix64_host(uint64_t z) {
@@ -806,16 +830,10 @@ static int check_lga(mdr_ctx* ctx, int method, const mdr_lga_settings* s) {
   return check_partition(ctx, s->partition, method);
 }
 
-mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, int method, int accum,
-                                    const mdr_lga_settings* s, int R) {
-  if (!ctx || !di || R <= 0) {
-    fail(ctx, MDR_ERR_INVALID, "bad argument");
-    return nullptr;
-  }
-  if (check_lga(ctx, method, s)) return nullptr;
-  if (di->grid && check_grid_block(ctx, di, s->partition)) return nullptr;
+// Device state of R runs with genotype stride `dim` (zero-initialised).
+static mdr_lga_batch* lga_batch_alloc(mdr_ctx* ctx, int method, int accum, const mdr_lga_settings* s, int R,
+                                      int dim) {
   mdr_lga_batch* b = new mdr_lga_batch;
-  b->L = di->view;
   b->method = method;
   b->pair = ctx->pair;
   b->accum = accum;
@@ -823,7 +841,7 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
   LgaDev& D = b->D;
   D.R = R;
   D.P = s->population_size;
-  D.dim = 6 + di->n_rot;
+  D.dim = dim;
   D.off = D.P - 1;
   D.L = ls_count_of(s);
   D.gens = s->generations;
@@ -835,23 +853,23 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
   D.tol = s->ls_convergence_tol;
   D.sigma = s->mutation_sigma;
   D.label_hash = label_hash("lga");
-  const size_t dim = D.dim, P = D.P, L = std::max(D.L, 1), Rr = R;
+  const size_t dm = D.dim, P = D.P, L = std::max(D.L, 1), Rr = R;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   size_t off = 0;
   std::vector<std::pair<void**, size_t>> parts;
   double *pop0, *pop1, *pe0, *pe1;
-  parts.push_back({(void**)&pop0, sizeof(double) * Rr * P * dim});
-  parts.push_back({(void**)&pop1, sizeof(double) * Rr * P * dim});
+  parts.push_back({(void**)&pop0, sizeof(double) * Rr * P * dm});
+  parts.push_back({(void**)&pop1, sizeof(double) * Rr * P * dm});
   parts.push_back({(void**)&pe0, sizeof(double) * Rr * P});
   parts.push_back({(void**)&pe1, sizeof(double) * Rr * P});
   parts.push_back({(void**)&D.cur, sizeof(int) * Rr});
-  parts.push_back({(void**)&D.lsg, sizeof(double) * Rr * L * dim});
+  parts.push_back({(void**)&D.lsg, sizeof(double) * Rr * L * dm});
   parts.push_back({(void**)&D.lse, sizeof(double) * Rr * L});
   parts.push_back({(void**)&D.lsit, sizeof(int) * Rr * L});
   parts.push_back({(void**)&D.lscv, sizeof(int) * Rr * L});
   parts.push_back({(void**)&D.lstarget, sizeof(int) * Rr * L});
   parts.push_back({(void**)&D.best_e, sizeof(double) * Rr});
-  parts.push_back({(void**)&D.best_g, sizeof(double) * Rr * dim});
+  parts.push_back({(void**)&D.best_g, sizeof(double) * Rr * dm});
   parts.push_back({(void**)&D.evals, sizeof(long long) * Rr});
   parts.push_back({(void**)&D.active, sizeof(int) * Rr});
   parts.push_back({(void**)&D.nrec, sizeof(int) * Rr});
@@ -860,8 +878,9 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
   parts.push_back({(void**)&D.status, sizeof(int) * Rr});
   parts.push_back({(void**)&b->seeds, sizeof(uint64_t) * Rr});
   for (auto& p : parts) off += al(p.second);
-  if (cudaMalloc(&b->block, off) != cudaSuccess) {
+  if (cudaMalloc(&b->block, off) != cudaSuccess || cudaMemset(b->block, 0, off) != cudaSuccess) {
     fail(ctx, MDR_ERR_CUDA, "cudaMalloc failed for LGA batch");
+    if (b->block) cudaFree(b->block);
     delete b;
     return nullptr;
   }
@@ -875,36 +894,70 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
   D.pope[0] = pe0;
   D.pope[1] = pe1;
   D.seeds = b->seeds;
-  // capture the whole docking (init, gens x {offspring, LS, finalize}, polish)
-  // into one CUDA graph, replayed per call
-  cudaStream_t cs;
-  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
-    fail(ctx, MDR_ERR_CUDA, "stream create failed");
-    cudaFree(b->block);
-    delete b;
+  return b;
+}
+
+static void lga_batch_release(mdr_lga_batch* b) {
+  if (b->exec) cudaGraphExecDestroy(b->exec);
+  if (b->graph) cudaGraphDestroy(b->graph);
+  if (b->gl_block) cudaFree(b->gl_block);
+  cudaFree(b->block);
+  delete b;
+}
+
+// Enqueue the whole docking of a batch on stream s (graph capture or a
+// profiling replay with events).
+static cudaError_t lga_batch_enqueue(mdr_lga_batch* b, cudaStream_t s, int wpb, int* launches,
+                                     cudaEvent_t* ev = nullptr) {
+  if (b->grid) return launch_grid_lga(b->GL, b->gsm, b->G, b->D, b->method, b->D.partition, s, launches, ev);
+  return launch_lga(b->L, b->D, b->method, b->pair, s, wpb, b->cta_warps, launches, ev);
+}
+
+mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, int method, int accum,
+                                    const mdr_lga_settings* s, int R) {
+  if (!ctx || !di || R <= 0) {
+    fail(ctx, MDR_ERR_INVALID, "bad argument");
     return nullptr;
   }
+  if (check_lga(ctx, method, s)) return nullptr;
+  if (di->grid && check_grid_block(ctx, di, s->partition)) return nullptr;
+  mdr_lga_batch* b = lga_batch_alloc(ctx, method, accum, s, R, 6 + di->n_rot);
+  if (!b) return nullptr;
+  b->L = di->view;
   b->cta_warps = cta_warps_for(ctx);
   b->grid = di->grid;
-  b->G = di->gview;
-  b->F = di->flex;
-  cudaError_t e = b->grid ? prepare_grid_lga(b->L, b->F, method, D.partition)
-                          : prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
+  cudaError_t e = cudaSuccess;
+  if (b->grid) {
+    b->G = di->gview;
+    e = cudaMalloc(&b->gl_block, 256 + sizeof(FlexView));
+    if (e == cudaSuccess) e = cudaMemcpy(b->gl_block, &di->view, sizeof(LigandView), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(static_cast<char*>(b->gl_block) + 256, &di->flex, sizeof(FlexView), cudaMemcpyHostToDevice);
+    b->GL.L = static_cast<const LigandView*>(b->gl_block);
+    b->GL.F = reinterpret_cast<const FlexView*>(static_cast<char*>(b->gl_block) + 256);
+    b->GL.run_lig = nullptr;
+    b->gsm = grid_smem_for(di->view, di->flex, s->partition);
+    if (e == cudaSuccess) e = prepare_grid_lga(b->gsm, method);
+  } else {
+    e = prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
+  }
+  // capture the whole docking (init, gens x {offspring, LS, finalize}, polish)
+  // into one CUDA graph, replayed per call
+  cudaStream_t cs = nullptr;
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
-  if (e == cudaSuccess)
-    e = b->grid ? launch_grid_lga(b->L, b->G, b->F, D, method, D.partition, cs, &b->launches)
-                : launch_lga(b->L, D, method, b->pair, cs, ctx->wpb, b->cta_warps, &b->launches);
-  cudaGraph_t g = nullptr;
-  cudaError_t e2 = cudaStreamEndCapture(cs, &g);
-  if (e == cudaSuccess) e = e2;
-  if (e == cudaSuccess) e = cudaGraphInstantiate(&b->exec, g, 0);
-  cudaStreamDestroy(cs);
-  b->graph = g;
+  if (e == cudaSuccess) {
+    e = lga_batch_enqueue(b, cs, ctx->wpb, &b->launches);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+    if (e == cudaSuccess) e = e2;
+    b->graph = g;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&b->exec, g, 0);
+  }
+  if (cs) cudaStreamDestroy(cs);
   if (e != cudaSuccess) {
     cuda_fail(ctx, e, "LGA graph capture");
-    if (g) cudaGraphDestroy(g);
-    cudaFree(b->block);
-    delete b;
+    lga_batch_release(b);
     return nullptr;
   }
   return b;
@@ -913,10 +966,7 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
 void mdr_lga_batch_destroy(mdr_ctx* ctx, mdr_lga_batch* b) {
   if (!b) return;
   if (ctx) cudaStreamSynchronize(ctx->stream);
-  if (b->exec) cudaGraphExecDestroy(b->exec);
-  if (b->graph) cudaGraphDestroy(b->graph);
-  cudaFree(b->block);
-  delete b;
+  lga_batch_release(b);
 }
 
 int mdr_lga_batch_run_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_seeds) {
@@ -936,10 +986,7 @@ int mdr_lga_batch_profile_dev(mdr_ctx* ctx, mdr_lga_batch* b, const uint64_t* d_
   for (auto& e : ev) CK(cudaEventCreate(&e));
   CK(cudaMemcpyAsync(b->seeds, d_seeds, sizeof(uint64_t) * D.R, cudaMemcpyDeviceToDevice, ctx->stream));
   int launches = 0;
-  if (b->grid)
-    CK(launch_grid_lga(b->L, b->G, b->F, D, b->method, D.partition, ctx->stream, &launches, ev.data()));
-  else
-    CK(launch_lga(b->L, D, b->method, b->pair, ctx->stream, ctx->wpb, b->cta_warps, &launches, ev.data()));
+  CK(lga_batch_enqueue(b, ctx->stream, ctx->wpb, &launches, ev.data()));
   ctx->launches += (uint64_t)launches;
   CK(cudaStreamSynchronize(ctx->stream));
   float tot = 0.f, t = 0.f;
@@ -1140,20 +1187,15 @@ void mdr_grid_free(mdr_ctx* ctx, mdr_dev_grid* d) {
 
 // Host preparation of the grid-mode chemistry (FlexView): per-atom
 // {radius, sqrt(epsilon), q, k_e q} and the torsion-group CSR.
-int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid* g, const mdr_ligand_params* p) {
-  if (!ctx || !di) return fail(ctx, MDR_ERR_INVALID, "bad argument");
-  if (!g) {
-    di->grid = false;
-    return MDR_OK;
-  }
+static int prep_flex(mdr_ctx* ctx, int na, int nr, const int* tors, const mdr_ligand_params* p, int n_types,
+                     std::vector<int>& type, std::vector<float4>& chem, std::vector<int>& off,
+                     std::vector<int>& members) {
   if (!p || !p->atom_type || !p->atom_charge || !p->atom_radius || !p->atom_epsilon)
     return fail(ctx, MDR_ERR_INVALID, "null ligand parameters");
-  const int na = di->n_atoms, nr = di->n_rot;
-  std::vector<int> tors(na), type(na);
-  CK(cudaMemcpy(tors.data(), di->view.tors, sizeof(int) * na, cudaMemcpyDeviceToHost));
-  std::vector<float4> chem(na);
+  type.assign(na, 0);
+  chem.assign(na, float4{});
   for (int i = 0; i < na; ++i) {
-    if (p->atom_type[i] < 0 || p->atom_type[i] >= g->view.n_types)
+    if (p->atom_type[i] < 0 || p->atom_type[i] >= n_types)
       return fail(ctx, MDR_ERR_SIZE, "atom type outside [0, n_types)");
     if (!(p->atom_epsilon[i] >= 0.0) || !std::isfinite(p->atom_charge[i]) || !std::isfinite(p->atom_radius[i]))
       return fail(ctx, MDR_ERR_NUMERIC_DOMAIN, "non-finite or negative ligand parameter");
@@ -1161,13 +1203,28 @@ int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid
     chem[i] = make_float4((float)p->atom_radius[i], (float)std::sqrt(p->atom_epsilon[i]), (float)p->atom_charge[i],
                           (float)(p->elec_scale * p->atom_charge[i]));
   }
-  std::vector<int> off(nr + 1, 0), members;
+  off.assign(nr + 1, 0);
+  members.clear();
   for (int k = 0; k < nr; ++k) {
     off[k] = (int)members.size();
     for (int i = 0; i < na; ++i)
       if (tors[i] == k) members.push_back(i);
   }
   off[nr] = (int)members.size();
+  return MDR_OK;
+}
+
+int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid* g, const mdr_ligand_params* p) {
+  if (!ctx || !di) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (!g) {
+    di->grid = false;
+    return MDR_OK;
+  }
+  const int na = di->n_atoms, nr = di->n_rot;
+  std::vector<int> tors(na), type, off, members;
+  std::vector<float4> chem;
+  CK(cudaMemcpy(tors.data(), di->view.tors, sizeof(int) * na, cudaMemcpyDeviceToHost));
+  if (int rc = prep_flex(ctx, na, nr, tors.data(), p, g->view.n_types, type, chem, off, members)) return rc;
   const int nta = (int)members.size();
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t o_type = 0, o_chem = al(sizeof(int) * na), o_off = o_chem + al(sizeof(float4) * na),
@@ -1295,6 +1352,266 @@ int mdr_grid_lga_run_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instan
   }
   mdr_lga_batch_destroy(ctx, b);
   return rc;
+}
+
+// ---------------------------------------------------------------- screen
+int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instance* ligs,
+                          const mdr_ligand_params* params, int n_lig, int runs, int method, const mdr_lga_settings* s,
+                          const uint64_t* seeds, double tol, double* best_e, double* best_g, int64_t* evals,
+                          int32_t* conv, int32_t* cluster_of, double* rmsd, int32_t* n_clusters) {
+  if (!ctx || !g || !ligs || !params || n_lig < 0 || runs < 0 || (n_lig && runs && !seeds))
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_lga(ctx, method, s)) return rc;
+  if (n_lig == 0 || runs == 0) return MDR_OK;
+  const int T = s->partition;
+  // ---- validate and pack every ligand into one host image of the device block
+  struct Lay {
+    size_t atoms, taxes, box, tors, type, chem, off, mem;
+    int na, nr, nta;
+  };
+  std::vector<Lay> lay(n_lig);
+  std::vector<char> img;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  auto put = [&](const void* src, size_t bytes, size_t reserve = 0) {  // reserve >= bytes of zeros
+    const size_t o = img.size();
+    img.resize(o + al(std::max(bytes, reserve)), 0);
+    if (bytes) std::memcpy(img.data() + o, src, bytes);
+    return o;
+  };
+  int max_dim = 6, max_na = 1;
+  size_t max_smem = 0;
+  for (int j = 0; j < n_lig; ++j) {
+    const mdr_instance* in = &ligs[j];
+    if (int rc = check_instance(ctx, in)) return rc;
+    Lay& L = lay[j];
+    L.na = in->n_atoms;
+    L.nr = in->n_rot;
+    if (T < 6 + L.nr) return fail(ctx, MDR_ERR_BLOCK_SIZE, "grid mode needs partition >= 6 + n_rot (one thread per dimension)");
+    std::vector<int> type, off, members;
+    std::vector<float4> chem;
+    if (int rc = prep_flex(ctx, L.na, L.nr, in->atom_torsion, &params[j], g->view.n_types, type, chem, off, members))
+      return rc;
+    L.nta = (int)members.size();
+    const size_t sm = grid_smem_for(L.na, L.nr, L.nta, T);
+    if (sm > 227 * 1024) return fail(ctx, MDR_ERR_SIZE, "grid-mode ligand does not fit in shared memory");
+    max_smem = std::max(max_smem, sm);
+    max_dim = std::max(max_dim, 6 + L.nr);
+    max_na = std::max(max_na, L.na);
+    std::vector<double> taxes(3 * (size_t)std::max(L.nr, 1), 0.0);
+    for (int k = 0; k < L.nr; ++k) torsion_axis_host(k, &taxes[3 * k]);
+    double box[6];
+    genotype_box(in, box);
+    L.atoms = put(in->atom_xyzw, sizeof(double) * 4 * L.na);
+    L.taxes = put(taxes.data(), sizeof(double) * taxes.size());
+    L.box = put(box, sizeof box);
+    L.tors = put(in->atom_torsion, sizeof(int) * L.na);
+    L.type = put(type.data(), sizeof(int) * L.na);
+    L.chem = put(chem.data(), sizeof(float4) * L.na);
+    L.off = put(off.data(), sizeof(int) * (L.nr + 1));
+    L.mem = put(members.data(), sizeof(int) * L.nta, sizeof(int));
+  }
+  const int R = n_lig * runs;
+  const size_t o_views = img.size();
+  img.resize(o_views + al(sizeof(LigandView) * n_lig) + al(sizeof(FlexView) * n_lig) + al(sizeof(int) * R) +
+                 al(sizeof(int) * (n_lig + 1)) + al(sizeof(int) * n_lig),
+             0);
+  const size_t o_flex = o_views + al(sizeof(LigandView) * n_lig), o_rl = o_flex + al(sizeof(FlexView) * n_lig),
+               o_seg = o_rl + al(sizeof(int) * R), o_segna = o_seg + al(sizeof(int) * (n_lig + 1));
+  mdr_lga_batch* b = lga_batch_alloc(ctx, method, MDR_ACCUM_SINGLE, s, R, max_dim);
+  if (!b) return MDR_ERR_CUDA;
+  struct Release {
+    mdr_ctx* ctx;
+    mdr_lga_batch* b;
+    ~Release() { mdr_lga_batch_destroy(ctx, b); }
+  } rel{ctx, b};
+  CK(cudaMalloc(&b->gl_block, img.size()));
+  char* base = static_cast<char*>(b->gl_block);
+  {
+    LigandView* lv = reinterpret_cast<LigandView*>(img.data() + o_views);
+    FlexView* fv = reinterpret_cast<FlexView*>(img.data() + o_flex);
+    int* rl = reinterpret_cast<int*>(img.data() + o_rl);
+    int* seg = reinterpret_cast<int*>(img.data() + o_seg);
+    int* segna = reinterpret_cast<int*>(img.data() + o_segna);
+    for (int j = 0; j < n_lig; ++j) {
+      const Lay& L = lay[j];
+      LigandView v{};
+      v.n_atoms = L.na;
+      v.n_sites = 0;
+      v.n_rot = L.nr;
+      v.atoms = reinterpret_cast<const double4*>(base + L.atoms);
+      v.taxes = reinterpret_cast<const double*>(base + L.taxes);
+      v.tors = reinterpret_cast<const int*>(base + L.tors);
+      v.box = reinterpret_cast<const double*>(base + L.box);
+      lv[j] = v;
+      FlexView f{};
+      f.type = reinterpret_cast<const int*>(base + L.type);
+      f.chem = reinterpret_cast<const float4*>(base + L.chem);
+      f.grp_off = reinterpret_cast<const int*>(base + L.off);
+      f.grp_atoms = reinterpret_cast<const int*>(base + L.mem);
+      f.n_tors_atoms = L.nta;
+      f.intra = params[j].intra != 0;
+      fv[j] = f;
+      for (int k = 0; k < runs; ++k) rl[j * runs + k] = j;
+      seg[j] = j * runs;
+      segna[j] = L.na;
+    }
+    seg[n_lig] = R;
+  }
+  CK(cudaMemcpyAsync(base, img.data(), img.size(), cudaMemcpyHostToDevice, S(ctx)));
+  b->grid = true;
+  b->G = g->view;
+  b->GL.L = reinterpret_cast<const LigandView*>(base + o_views);
+  b->GL.F = reinterpret_cast<const FlexView*>(base + o_flex);
+  b->GL.run_lig = reinterpret_cast<const int*>(base + o_rl);
+  b->gsm = max_smem;
+  CK(prepare_grid_lga(b->gsm, method));
+  CK(cudaMemcpyAsync(b->seeds, seeds, sizeof(uint64_t) * R, cudaMemcpyHostToDevice, S(ctx)));
+  int launches = 0;
+  CK(lga_batch_enqueue(b, S(ctx), ctx->wpb, &launches));
+  ctx->launches += (uint64_t)launches;
+  // ---- per-ligand clustering of the best poses (one CTA per ligand)
+  DevBuf<double> xyz, dr;
+  DevBuf<int> dc, dn, order, sd;
+  if (cluster_of || rmsd || n_clusters) {
+    CK(xyz.alloc((size_t)R * 3 * max_na, S(ctx)));
+    CK(dr.alloc(R, S(ctx)));
+    CK(dc.alloc(R, S(ctx)));
+    CK(dn.alloc(n_lig, S(ctx)));
+    CK(order.alloc(R, S(ctx)));
+    CK(sd.alloc(R, S(ctx)));
+    CK(launch_pose_coords(b->GL.L, b->GL.run_lig, b->D.best_g, b->D.dim, R, 3ll * max_na, xyz.p, S(ctx)));
+    CK(launch_cluster(xyz.p, 3ll * max_na, b->D.best_e, reinterpret_cast<const int*>(base + o_seg),
+                      reinterpret_cast<const int*>(base + o_segna), n_lig, max_na, tol, dc.p, dr.p, dn.p, order.p,
+                      sd.p, S(ctx)));
+    ctx->launches += 2;
+  }
+  // ---- results
+  std::vector<double> bg((size_t)R * b->D.dim);
+  std::vector<int> status(R);
+  std::vector<long long> ev(R);
+  if (best_e) CK(cudaMemcpyAsync(best_e, b->D.best_e, sizeof(double) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (best_g) CK(cudaMemcpyAsync(bg.data(), b->D.best_g, sizeof(double) * bg.size(), cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(ev.data(), b->D.evals, sizeof(long long) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (conv) CK(cudaMemcpyAsync(conv, b->D.conv, sizeof(int) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(status.data(), b->D.status, sizeof(int) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (cluster_of) CK(cudaMemcpyAsync(cluster_of, dc.p, sizeof(int) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (rmsd) CK(cudaMemcpyAsync(rmsd, dr.p, sizeof(double) * R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (n_clusters) CK(cudaMemcpyAsync(n_clusters, dn.p, sizeof(int) * n_lig, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  if (evals)
+    for (int r = 0; r < R; ++r) evals[r] = ev[r];
+  if (best_g) {
+    size_t o = 0;
+    for (int j = 0; j < n_lig; ++j) {
+      const int dim = 6 + lay[j].nr;
+      for (int k = 0; k < runs; ++k, o += dim)
+        std::memcpy(best_g + o, bg.data() + (size_t)(j * runs + k) * b->D.dim, sizeof(double) * dim);
+    }
+  }
+  for (int r = 0; r < R; ++r)
+    if (status[r] != MDR_OK) return fail(ctx, status[r], "adadelta_step: non-finite gradient component");
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------- clustering
+int mdr_cluster_segments_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* genos, const double* energy,
+                             const int32_t* seg_off, int n_seg, int n_total, double tol, int32_t* cluster_of,
+                             double* rmsd, int32_t* n_clusters) {
+  if (!ctx || !di || n_seg < 0 || n_total < 0 || !(tol >= 0.0)) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (n_seg == 0 || n_total == 0) return MDR_OK;
+  DevBuf<double> xyz;
+  DevBuf<int> order, seeds;
+  DevBuf<LigandView> lv;
+  CK(xyz.alloc((size_t)n_total * 3 * di->n_atoms, S(ctx)));
+  CK(order.alloc(n_total, S(ctx)));
+  CK(seeds.alloc(n_total, S(ctx)));
+  CK(lv.alloc(1, S(ctx)));
+  CK(cudaMemcpyAsync(lv.p, &di->view, sizeof(LigandView), cudaMemcpyHostToDevice, S(ctx)));
+  const long long xs = 3ll * di->n_atoms;
+  CK(launch_pose_coords(lv.p, nullptr, genos, 6 + di->n_rot, n_total, xs, xyz.p, S(ctx)));
+  CK(launch_cluster(xyz.p, xs, energy, seg_off, nullptr, n_seg, di->n_atoms, tol, cluster_of, rmsd, n_clusters,
+                    order.p, seeds.p, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));  // the staged view dies at return
+  ctx->launches += 2;
+  return MDR_OK;
+}
+
+int mdr_pose_coords_batch(mdr_ctx* ctx, const mdr_instance* inst, const double* genos, int n, double* xyz) {
+  if (!ctx || n < 0 || (n && (!genos || !xyz))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  if (n == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> dg, dx;
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(dx.alloc((size_t)n * 3 * inst->n_atoms, S(ctx)));
+  CK(cudaMemcpyAsync(dg.p, genos, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  DevBuf<LigandView> lv;
+  CK(lv.alloc(1, S(ctx)));
+  CK(cudaMemcpyAsync(lv.p, &ig.di->view, sizeof(LigandView), cudaMemcpyHostToDevice, S(ctx)));
+  CK(launch_pose_coords(lv.p, nullptr, dg.p, dim, n, 3ll * inst->n_atoms, dx.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(xyz, dx.p, sizeof(double) * n * 3 * inst->n_atoms, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_cluster_poses(mdr_ctx* ctx, const mdr_instance* inst, const double* genos, const double* energies, int n,
+                      double tol, int32_t* cluster_of, double* rmsd, int32_t* n_clusters) {
+  if (!ctx || n < 0 || !n_clusters || (n && (!genos || !energies || !cluster_of))) 
+    return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (!(tol >= 0.0)) return fail(ctx, MDR_ERR_INVALID, "rmsd tolerance must be >= 0");
+  if (int rc = check_instance(ctx, inst)) return rc;
+  *n_clusters = 0;
+  if (n == 0) return MDR_OK;
+  InstanceGuard ig{ctx, mdr_instance_upload(ctx, inst)};
+  if (!ig.di) return MDR_ERR_CUDA;
+  const int dim = 6 + inst->n_rot;
+  DevBuf<double> dg, de, dr;
+  DevBuf<int> dc, dn, doff;
+  CK(dg.alloc((size_t)n * dim, S(ctx)));
+  CK(de.alloc(n, S(ctx)));
+  CK(dr.alloc(n, S(ctx)));
+  CK(dc.alloc(n, S(ctx)));
+  CK(dn.alloc(1, S(ctx)));
+  CK(doff.alloc(2, S(ctx)));
+  const int off[2] = {0, n};
+  CK(cudaMemcpyAsync(dg.p, genos, sizeof(double) * n * dim, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(de.p, energies, sizeof(double) * n, cudaMemcpyHostToDevice, S(ctx)));
+  CK(cudaMemcpyAsync(doff.p, off, sizeof off, cudaMemcpyHostToDevice, S(ctx)));
+  if (int rc = mdr_cluster_segments_dev(ctx, ig.di, dg.p, de.p, doff.p, 1, n, tol, dc.p, dr.p, dn.p)) return rc;
+  CK(cudaMemcpyAsync(cluster_of, dc.p, sizeof(int) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  if (rmsd) CK(cudaMemcpyAsync(rmsd, dr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(n_clusters, dn.p, sizeof(int), cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_lga_batch_cluster(mdr_ctx* ctx, mdr_lga_batch* b, double tol, int32_t* cluster_of, double* rmsd,
+                          int32_t* n_clusters) {
+  if (!ctx || !b || !cluster_of || !n_clusters) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  const LgaDev& D = b->D;
+  mdr_dev_instance view;  // the batch's ligand (LigandView copy; nothing owned)
+  view.view = b->L;
+  view.n_atoms = b->L.n_atoms;
+  view.n_rot = b->L.n_rot;
+  DevBuf<double> dr;
+  DevBuf<int> dc, dn, doff;
+  CK(dr.alloc(D.R, S(ctx)));
+  CK(dc.alloc(D.R, S(ctx)));
+  CK(dn.alloc(1, S(ctx)));
+  CK(doff.alloc(2, S(ctx)));
+  const int off[2] = {0, D.R};
+  CK(cudaMemcpyAsync(doff.p, off, sizeof off, cudaMemcpyHostToDevice, S(ctx)));
+  int rc = mdr_cluster_segments_dev(ctx, &view, D.best_g, D.best_e, doff.p, 1, D.R, tol, dc.p, dr.p, dn.p);
+  view.block = nullptr;
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(cluster_of, dc.p, sizeof(int) * D.R, cudaMemcpyDeviceToHost, S(ctx)));
+  if (rmsd) CK(cudaMemcpyAsync(rmsd, dr.p, sizeof(double) * D.R, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaMemcpyAsync(n_clusters, dn.p, sizeof(int), cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
 }
 
 }  // extern "C"

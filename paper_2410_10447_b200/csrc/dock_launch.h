@@ -32,12 +32,20 @@ cudaError_t launch_grid_score(const LigandView& L, const GridView& G, const Flex
 cudaError_t launch_grid_local_search(const LigandView& L, const GridView& G, const FlexView& F, const double* starts,
                                      int n, int max_iters, double tol, int method, int threads, double* out_g,
                                      double* out_e, int* out_it, int* out_cv, int* status, cudaStream_t s);
-cudaError_t prepare_grid_lga(const LigandView& L, const FlexView& F, int method, int threads);
-cudaError_t launch_grid_lga(const LigandView& L, const GridView& G, const FlexView& F, const LgaDev& D, int method,
+size_t grid_smem_for(int n_atoms, int n_rot, int n_tors_atoms, int threads);
+cudaError_t prepare_grid_lga(size_t smem, int method);
+cudaError_t launch_grid_lga(const GridLigands& GL, size_t smem, const GridView& G, const LgaDev& D, int method,
                             int threads, cudaStream_t s, int* n_launches, cudaEvent_t* ls_events = nullptr);
 cudaError_t launch_grid_build(const GridView& G, const double* sites, int n_sites, const double* charge,
                               const double* volume, const double* depth_scale, const double* dist_scale,
                               double elec_scale, double sigma, float* maps, cudaStream_t s);
+
+// cluster.cu (RMSD clustering)
+cudaError_t launch_pose_coords(const LigandView* Ls, const int* pose_lig, const double* genos, int gstride, int n,
+                               long long xstride, double* xyz, cudaStream_t s);
+cudaError_t launch_cluster(const double* xyz, long long xstride, const double* energy, const int* seg_off,
+                           const int* seg_na, int n_seg, int na, double tol, int* cluster_of, double* rmsd,
+                           int* n_clusters, int* order, int* seeds, cudaStream_t s);
 
 // reduce.cu
 cudaError_t launch_f32_to_half(const float* in, size_t n, uint16_t* out, cudaStream_t s);

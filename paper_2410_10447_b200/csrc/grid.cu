@@ -463,17 +463,28 @@ __global__ void grid_ls_kernel(LigandView L, GridView G, FlexView F, const doubl
 }
 
 // ------------------------------------------------------------- LGA phases
+// All phases take a GridLigands table: a batch docks one ligand (n = 1) or
+// a virtual-screen batch of many (run r docks ligand run_lig[r]).  D.dim is
+// the genotype stride (the batch's largest dimension); each run uses its
+// own ligand's dimension, and its RNG draw offsets (docking.cpp:437-465)
+// follow that dimension exactly as a single-ligand lga_run would.
+__device__ __forceinline__ int run_ligand(const GridLigands& GL, int run) { return GL.run_lig ? GL.run_lig[run] : 0; }
+
 // random_genotype docking.cpp:360-388 + score, CTA per individual.
 template <int METHOD>
-__global__ void grid_lga_init_kernel(LigandView L, GridView G, FlexView F, LgaDev D) {
+__global__ void grid_lga_init_kernel(GridLigands GL, GridView G, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const GridSmem S = grid_load(L, F, smem);
   const int item = blockIdx.x;
   const int run = item / D.P, p = item % D.P;
+  const int lig = run_ligand(GL, run);
+  const LigandView L = GL.L[lig];
+  const FlexView F = GL.F[lig];
+  const GridSmem S = grid_load(L, F, smem);
+  const int dim = 6 + L.n_rot;
   const int d = threadIdx.x;
-  if (d < D.dim) {
+  if (d < dim) {
     const uint64_t key = run_key(D, run);
-    const uint64_t n = (uint64_t)p * D.dim + d + 1;
+    const uint64_t n = (uint64_t)p * dim + d + 1;
     const double x = d < 3 ? L.box[d] + (L.box[3 + d] - L.box[d]) * draw_unit(key, n)
                            : -kPi + (kPi - -kPi) * draw_unit(key, n);
     S.g[d] = x;
@@ -487,12 +498,16 @@ __global__ void grid_lga_init_kernel(LigandView L, GridView G, FlexView F, LgaDe
 
 // Offspring (docking.cpp:437-472), CTA per child; thread d forms dimension d.
 template <int METHOD>
-__global__ void grid_lga_offspring_kernel(LigandView L, GridView G, FlexView F, LgaDev D, int gen) {
+__global__ void grid_lga_offspring_kernel(GridLigands GL, GridView G, LgaDev D, int gen) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const GridSmem S = grid_load(L, F, smem);
   const int item = blockIdx.x;
   const int run = item / D.off, i = item % D.off;
   if (!D.active[run]) return;  // uniform over the CTA
+  const int lig = run_ligand(GL, run);
+  const LigandView L = GL.L[lig];
+  const FlexView F = GL.F[lig];
+  const GridSmem S = grid_load(L, F, smem);
+  const int dim = 6 + L.n_rot;
   const int c = D.cur[run];
   const double* pop = D.pop[c] + (size_t)run * D.P * D.dim;
   const double* pe = D.pope[c] + (size_t)run * D.P;
@@ -506,13 +521,13 @@ __global__ void grid_lga_offspring_kernel(LigandView L, GridView G, FlexView F, 
         be = pe[p];
         bi = p;
       }
-    for (int d = threadIdx.x; d < D.dim; d += 32) nxt[d] = pop[(size_t)bi * D.dim + d];
+    for (int d = threadIdx.x; d < dim; d += 32) nxt[d] = pop[(size_t)bi * D.dim + d];
     if (threadIdx.x == 0) ne[0] = be;
   }
   const uint64_t key = run_key(D, run);
-  const uint64_t base = (uint64_t)D.P * D.dim + ((uint64_t)gen * D.off + i) * (uint64_t)(4 + 3 * D.dim);
+  const uint64_t base = (uint64_t)D.P * dim + ((uint64_t)gen * D.off + i) * (uint64_t)(4 + 3 * dim);
   const int d = threadIdx.x;
-  if (d < D.dim) {
+  if (d < dim) {
     const int ia = (int)(draw_u64(key, base + 1) % (uint64_t)D.P);
     const int ja = (int)(draw_u64(key, base + 2) % (uint64_t)D.P);
     const int a = pe[ia] <= pe[ja] ? ia : ja;
@@ -521,7 +536,7 @@ __global__ void grid_lga_offspring_kernel(LigandView L, GridView G, FlexView F, 
     const int b = pe[ib] <= pe[jb] ? ib : jb;
     const double lam = draw_unit(key, base + 5 + d);
     double x = lam * pop[(size_t)a * D.dim + d] + (1.0 - lam) * pop[(size_t)b * D.dim + d];
-    x = x + D.sigma * draw_normal(key, base + 5 + D.dim + 2 * (uint64_t)d);
+    x = x + D.sigma * draw_normal(key, base + 5 + dim + 2 * (uint64_t)d);
     if (d >= 3) x = wrap_angle(x);
     S.g[d] = x;
     nxt[(size_t)(1 + i) * D.dim + d] = x;
@@ -533,13 +548,17 @@ __global__ void grid_lga_offspring_kernel(LigandView L, GridView G, FlexView F, 
 }
 
 template <int METHOD>
-__global__ void grid_lga_ls_kernel(LigandView L, GridView G, FlexView F, LgaDev D) {
+__global__ void grid_lga_ls_kernel(GridLigands GL, GridView G, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const GridSmem S = grid_load(L, F, smem);
   __shared__ int s_target;
   const int item = blockIdx.x;
   const int run = item / D.L, r = item % D.L;
   if (!D.active[run]) return;
+  const int lig = run_ligand(GL, run);
+  const LigandView L = GL.L[lig];
+  const FlexView F = GL.F[lig];
+  const GridSmem S = grid_load(L, F, smem);
+  const int dim = 6 + L.n_rot;
   if (threadIdx.x < 32) {
     const int t = ls_target(D, run, r);
     if (threadIdx.x == 0) s_target = t;
@@ -550,7 +569,7 @@ __global__ void grid_lga_ls_kernel(LigandView L, GridView G, FlexView F, LgaDev 
   const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
   const GridLs res = grid_local_search<METHOD>(S, G, F.intra != 0, start, D.ls_iters, D.tol);
   const size_t o = (size_t)run * D.L + r;
-  if (threadIdx.x < D.dim) D.lsg[o * D.dim + threadIdx.x] = S.best[threadIdx.x];
+  if (threadIdx.x < dim) D.lsg[o * D.dim + threadIdx.x] = S.best[threadIdx.x];
   if (threadIdx.x == 0) {
     D.lse[o] = res.energy;
     D.lsit[o] = res.iterations;
@@ -562,11 +581,14 @@ __global__ void grid_lga_ls_kernel(LigandView L, GridView G, FlexView F, LgaDev 
 
 // Final polish from the incumbent best (docking.cpp:501-515), CTA per run.
 template <int METHOD>
-__global__ void grid_lga_polish_kernel(LigandView L, GridView G, FlexView F, LgaDev D) {
+__global__ void grid_lga_polish_kernel(GridLigands GL, GridView G, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int run = blockIdx.x;
+  const int lig = run_ligand(GL, run);
+  const LigandView L = GL.L[lig];
+  const FlexView F = GL.F[lig];
   const GridSmem S = grid_load(L, F, smem);
   __syncthreads();
-  const int run = blockIdx.x;
   if (D.status[run] != MDR_OK) return;
   const long long remaining = D.max_evals - D.evals[run];
   if (remaining <= 1) {
@@ -657,6 +679,9 @@ static size_t gsmem(const LigandView& L, const FlexView& F, int T) {
 }
 
 size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads) { return gsmem(L, F, threads); }
+size_t grid_smem_for(int n_atoms, int n_rot, int n_tors_atoms, int threads) {
+  return grid_smem_bytes(n_atoms, n_rot, n_tors_atoms, threads);
+}
 
 cudaError_t launch_grid_score(const LigandView& L, const GridView& G, const FlexView& F, const double* genos, int n,
                               int method, int threads, float* energy, float* grad, float* torque, cudaStream_t s) {
@@ -680,8 +705,7 @@ cudaError_t launch_grid_local_search(const LigandView& L, const GridView& G, con
   return cudaGetLastError();
 }
 
-cudaError_t prepare_grid_lga(const LigandView& L, const FlexView& F, int method, int threads) {
-  const size_t sm = gsmem(L, F, threads);
+cudaError_t prepare_grid_lga(size_t sm, int method) {
   cudaError_t e = gprep_grid_lga_init_kernel(method, sm);
   if (e == cudaSuccess) e = gprep_grid_lga_offspring_kernel(method, sm);
   if (e == cudaSuccess) e = gprep_grid_lga_ls_kernel(method, sm);
@@ -689,25 +713,24 @@ cudaError_t prepare_grid_lga(const LigandView& L, const FlexView& F, int method,
   return e;
 }
 
-cudaError_t launch_grid_lga(const LigandView& L, const GridView& G, const FlexView& F, const LgaDev& D, int method,
+cudaError_t launch_grid_lga(const GridLigands& GL, size_t sm, const GridView& G, const LgaDev& D, int method,
                             int threads, cudaStream_t s, int* n_launches, cudaEvent_t* ls_events) {
-  const size_t sm = gsmem(L, F, threads);
   int launches = 0;
   cudaError_t e = cudaSuccess;
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 2], s);
-  gdispatch_grid_lga_init_kernel(method, D.R * D.P, threads, sm, s, L, G, F, D);
+  gdispatch_grid_lga_init_kernel(method, D.R * D.P, threads, sm, s, GL, G, D);
   if ((e = launch_lga_init_finalize(D, s)) != cudaSuccess) return e;
   launches += 2;
   for (int gen = 0; gen < D.gens; ++gen) {
-    gdispatch_grid_lga_offspring_kernel(method, D.R * D.off, threads, sm, s, L, G, F, D, gen);
+    gdispatch_grid_lga_offspring_kernel(method, D.R * D.off, threads, sm, s, GL, G, D, gen);
     if (ls_events) cudaEventRecord(ls_events[2 * gen], s);
-    if (D.L > 0) gdispatch_grid_lga_ls_kernel(method, D.R * D.L, threads, sm, s, L, G, F, D);
+    if (D.L > 0) gdispatch_grid_lga_ls_kernel(method, D.R * D.L, threads, sm, s, GL, G, D);
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
     if ((e = launch_lga_gen_finalize(D, gen, s)) != cudaSuccess) return e;
     launches += D.L > 0 ? 3 : 2;
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
-  gdispatch_grid_lga_polish_kernel(method, D.R, threads, sm, s, L, G, F, D);
+  gdispatch_grid_lga_polish_kernel(method, D.R, threads, sm, s, GL, G, D);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;

@@ -57,6 +57,15 @@ struct FlexView {
   int n_tors_atoms, intra;
 };
 
+// Per-run ligand tables of a grid-mode LGA batch (device arrays): one
+// ligand (run_lig == nullptr) or a virtual-screen batch (run r docks ligand
+// run_lig[r]).
+struct GridLigands {
+  const LigandView* L;
+  const FlexView* F;
+  const int* run_lig;
+};
+
 // All device state of a batch of LGA runs (docking.cpp:392-517).
 struct LgaDev {
   int R, P, dim, off, L, gens, ls_iters, maxrec, partition, half_mode;
