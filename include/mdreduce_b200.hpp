@@ -17,6 +17,7 @@
 #include <string>
 #include <string_view>
 #include <utility>
+#include <memory>
 #include <vector>
 
 namespace mdreduce {
@@ -323,6 +324,82 @@ std::vector<LocalSearchResult> local_search_batch(const LigandInstance& instance
                                                   AccumMode accum_mode, int partition);
 std::vector<DockResult> lga_run_batch(const LigandInstance& instance, ReduceMethod method, AccumMode accum_mode,
                                       const LgaSettings& settings, const std::vector<std::uint64_t>& seeds);
+
+// ---- grid-map scoring mode (formulas in include/mdr.h) -------
+struct GridShape {
+  int nx = 2, ny = 2, nz = 2, n_types = 1;
+  std::array<double, 3> origin{0.0, 0.0, 0.0};
+  double spacing = 0.375;
+};
+// Maps (n_types + 2) x nz x ny x nx, x fastest: type maps, elec, desolv.
+struct GridMaps {
+  GridShape shape;
+  std::vector<float> maps;
+};
+// Synthetic receptor chemistry for the map builder (mdr_receptor_fields).
+struct ReceptorFields {
+  std::vector<double> site_charge, site_volume, type_depth_scale, type_dist_scale;
+  double elec_scale = 83.0;
+  double desolv_sigma = 3.6;
+};
+// Per-atom ligand chemistry (mdr_ligand_params).
+struct LigandChemistry {
+  std::vector<int> atom_type;
+  std::vector<double> charge, radius, epsilon;
+  double elec_scale = 83.0;
+  bool intra = true;
+};
+// A device-resident receptor (maps uploaded once, shared by every ligand).
+class Receptor {
+ public:
+  static Receptor upload(const GridMaps& maps);
+  // maps computed on the device from the sites of `sites`
+  static Receptor build(const LigandInstance& sites, const ReceptorFields& fields, const GridShape& shape);
+  GridMaps download() const;
+  const GridShape& shape() const { return shape_; }
+  void* handle() const { return handle_.get(); }
+
+ private:
+  GridShape shape_;
+  std::shared_ptr<void> handle_;
+};
+// Energy, exact gradient (per-group torsion torque), inter torque per pose;
+// reduce_stats are zero (no reference model counters for this mode).
+std::vector<ScoreResult> grid_score_batch(const Receptor& receptor, const LigandInstance& ligand,
+                                          const LigandChemistry& chem, const std::vector<Genotype>& poses,
+                                          ReduceMethod method, int partition);
+std::vector<LocalSearchResult> grid_local_search_batch(const Receptor& receptor, const LigandInstance& ligand,
+                                                       const LigandChemistry& chem,
+                                                       const std::vector<Genotype>& starts, int max_iters,
+                                                       double convergence_tol, ReduceMethod method, int partition);
+std::vector<DockResult> grid_lga_run_batch(const Receptor& receptor, const LigandInstance& ligand,
+                                           const LigandChemistry& chem, ReduceMethod method,
+                                           const LgaSettings& settings, const std::vector<std::uint64_t>& seeds);
+
+// ---- RMSD clustering ----------------------------------------
+struct Clustering {
+  std::vector<int> cluster_of;        // cluster index per pose (0 = best pose's)
+  std::vector<double> rmsd_to_seed;   // RMSD to the cluster's lowest-energy pose
+  int n_clusters = 0;
+};
+std::vector<std::array<double, 3>> pose_coordinates(const LigandInstance& ligand, const Genotype& pose);
+Clustering cluster_poses(const LigandInstance& ligand, const std::vector<Genotype>& poses,
+                         const std::vector<double>& energies, double rmsd_tol);
+
+// ---- virtual screen ------------------------------------------
+struct ScreenResult {
+  std::vector<double> best_energy;
+  std::vector<Genotype> best_genotype;
+  std::vector<std::int64_t> evaluations;
+  std::vector<bool> converged;
+  Clustering clusters;
+};
+// Every ligand docked runs_per_ligand times (seeds[j * runs + k]) in one
+// launch sequence, then its best poses clustered.
+std::vector<ScreenResult> screen_batch(const Receptor& receptor, const std::vector<LigandInstance>& ligands,
+                                       const std::vector<LigandChemistry>& chemistry, int runs_per_ligand,
+                                       ReduceMethod method, const LgaSettings& settings,
+                                       const std::vector<std::uint64_t>& seeds, double rmsd_tol);
 }  // namespace b200
 
 }  // namespace mdreduce

@@ -507,6 +507,229 @@ std::vector<DockResult> lga_run_batch(const LigandInstance& in, ReduceMethod met
   return out;
 }
 
+// ---------------------------------------------------------------- grid mode
+namespace {
+mdr_grid grid_to_c(const GridShape& g, const float* maps) {
+  mdr_grid o{};
+  o.nx = g.nx;
+  o.ny = g.ny;
+  o.nz = g.nz;
+  o.n_types = g.n_types;
+  o.origin[0] = g.origin[0];
+  o.origin[1] = g.origin[1];
+  o.origin[2] = g.origin[2];
+  o.spacing = g.spacing;
+  o.maps = maps;
+  return o;
+}
+
+struct FlatChem {  // mdr_ligand_params view of a LigandChemistry
+  mdr_ligand_params c{};
+  explicit FlatChem(const LigandInstance& in, const LigandChemistry& ch) {
+    const std::size_t n = in.atoms.size();
+    if (ch.atom_type.size() != n || ch.charge.size() != n || ch.radius.size() != n || ch.epsilon.size() != n)
+      throw SizeError("ligand chemistry needs one entry per atom");
+    c.atom_type = reinterpret_cast<const int32_t*>(ch.atom_type.data());
+    c.atom_charge = ch.charge.data();
+    c.atom_radius = ch.radius.data();
+    c.atom_epsilon = ch.epsilon.data();
+    c.elec_scale = ch.elec_scale;
+    c.intra = ch.intra ? 1 : 0;
+  }
+};
+
+std::shared_ptr<void> grid_handle(mdr_dev_grid* h) {
+  if (!h) check(MDR_ERR_CUDA);
+  return std::shared_ptr<void>(h, [](void* p) { mdr_grid_free(nullptr, static_cast<mdr_dev_grid*>(p)); });
+}
+
+mdr_dev_grid* dev_grid(const Receptor& r) { return static_cast<mdr_dev_grid*>(r.handle()); }
+}  // namespace
+
+Receptor Receptor::upload(const GridMaps& m) {
+  const std::size_t need = static_cast<std::size_t>(m.shape.n_types + 2) * m.shape.nx * m.shape.ny * m.shape.nz;
+  if (m.maps.size() != need) throw SizeError("grid maps need (n_types + 2) * nx * ny * nz values");
+  const mdr_grid g = grid_to_c(m.shape, m.maps.data());
+  Receptor r;
+  r.shape_ = m.shape;
+  mdr_dev_grid* h = mdr_grid_upload(ctx(), &g);
+  if (!h) check(MDR_ERR_SIZE);
+  r.handle_ = grid_handle(h);
+  return r;
+}
+
+Receptor Receptor::build(const LigandInstance& sites, const ReceptorFields& f, const GridShape& shape) {
+  if (f.site_charge.size() != sites.sites.size() || f.site_volume.size() != sites.sites.size() ||
+      static_cast<int>(f.type_depth_scale.size()) != shape.n_types ||
+      static_cast<int>(f.type_dist_scale.size()) != shape.n_types)
+    throw SizeError("receptor fields need one entry per site / type");
+  FlatInstance fi(sites);
+  mdr_receptor_fields c{f.site_charge.data(), f.site_volume.data(), f.type_depth_scale.data(),
+                        f.type_dist_scale.data(), f.elec_scale, f.desolv_sigma};
+  const mdr_grid g = grid_to_c(shape, nullptr);
+  Receptor r;
+  r.shape_ = shape;
+  mdr_dev_grid* h = mdr_grid_build(ctx(), &fi.c, &c, &g);
+  if (!h) check(MDR_ERR_SIZE);
+  r.handle_ = grid_handle(h);
+  return r;
+}
+
+GridMaps Receptor::download() const {
+  GridMaps m;
+  m.shape = shape_;
+  m.maps.resize(static_cast<std::size_t>(shape_.n_types + 2) * shape_.nx * shape_.ny * shape_.nz);
+  check(mdr_grid_download(ctx(), dev_grid(*this), m.maps.data()));
+  return m;
+}
+
+std::vector<ScoreResult> grid_score_batch(const Receptor& rec, const LigandInstance& in, const LigandChemistry& ch,
+                                          const std::vector<Genotype>& poses, ReduceMethod method, int partition) {
+  for (const Genotype& g : poses) check_genotype(in, g, "score");
+  FlatInstance fi(in);
+  FlatChem fc(in, ch);
+  const int n = static_cast<int>(poses.size()), dim = 6 + in.n_rot;
+  const std::vector<double> g = flat_genotypes(poses);
+  std::vector<float> e(n), grad(static_cast<std::size_t>(n) * dim), tq(3 * static_cast<std::size_t>(n));
+  check(mdr_grid_score_batch(ctx(), dev_grid(rec), &fi.c, &fc.c, g.data(), n, method_id(method), partition, e.data(),
+                             grad.data(), tq.data()));
+  std::vector<ScoreResult> out(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    ScoreResult& r = out[static_cast<std::size_t>(i)];
+    r.energy = e[i];
+    r.gradient.assign(grad.begin() + static_cast<std::ptrdiff_t>(i) * dim,
+                      grad.begin() + static_cast<std::ptrdiff_t>(i + 1) * dim);
+    r.torque = {tq[3 * i], tq[3 * i + 1], tq[3 * i + 2]};
+  }
+  return out;
+}
+
+std::vector<LocalSearchResult> grid_local_search_batch(const Receptor& rec, const LigandInstance& in,
+                                                       const LigandChemistry& ch, const std::vector<Genotype>& starts,
+                                                       int max_iters, double tol, ReduceMethod method, int partition) {
+  for (const Genotype& g : starts) check_genotype(in, g, "score");
+  FlatInstance fi(in);
+  FlatChem fc(in, ch);
+  const int n = static_cast<int>(starts.size()), dim = 6 + in.n_rot;
+  const std::vector<double> s = flat_genotypes(starts);
+  std::vector<double> og(s.size()), oe(static_cast<std::size_t>(n));
+  std::vector<int32_t> it(static_cast<std::size_t>(n)), cv(static_cast<std::size_t>(n));
+  check(mdr_grid_local_search_batch(ctx(), dev_grid(rec), &fi.c, &fc.c, s.data(), n, max_iters, tol,
+                                    method_id(method), partition, og.data(), oe.data(), it.data(), cv.data()));
+  std::vector<LocalSearchResult> out(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    LocalSearchResult& r = out[static_cast<std::size_t>(i)];
+    r.genotype = make_genotype(og.data() + static_cast<std::ptrdiff_t>(i) * dim, in.n_rot);
+    r.energy = oe[i];
+    r.iterations = it[i];
+    r.converged = cv[i] != 0;
+  }
+  return out;
+}
+
+std::vector<DockResult> grid_lga_run_batch(const Receptor& rec, const LigandInstance& in, const LigandChemistry& ch,
+                                           ReduceMethod method, const LgaSettings& settings,
+                                           const std::vector<std::uint64_t>& seeds) {
+  FlatInstance fi(in);
+  FlatChem fc(in, ch);
+  const mdr_lga_settings cs = to_c(settings);
+  if (settings.population_size < 2) throw SizeError("lga_run needs a population of at least 2");
+  const int n = static_cast<int>(seeds.size()), dim = 6 + in.n_rot, maxr = mdr_lga_max_records(&cs);
+  std::vector<double> be(static_cast<std::size_t>(n)), bg(static_cast<std::size_t>(n) * dim);
+  std::vector<int64_t> ev(static_cast<std::size_t>(n));
+  std::vector<int32_t> cv(static_cast<std::size_t>(n)), nr(static_cast<std::size_t>(n));
+  std::vector<mdr_ls_record> recs(static_cast<std::size_t>(n) * maxr);
+  check(mdr_grid_lga_run_batch(ctx(), dev_grid(rec), &fi.c, &fc.c, method_id(method), &cs, seeds.data(), n,
+                               be.data(), bg.data(), ev.data(), cv.data(), nr.data(), recs.data()));
+  std::vector<DockResult> out(static_cast<std::size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    DockResult& r = out[static_cast<std::size_t>(i)];
+    r.best_energy = be[i];
+    r.best_genotype = make_genotype(bg.data() + static_cast<std::ptrdiff_t>(i) * dim, in.n_rot);
+    r.evaluations = ev[i];
+    r.converged = cv[i] != 0;
+    for (int k = 0; k < std::min<int>(nr[i], maxr); ++k) {
+      const mdr_ls_record& q = recs[static_cast<std::size_t>(i) * maxr + k];
+      r.runs.push_back(LsRunRecord{q.best_energy, q.iterations, q.converged != 0});
+    }
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- clustering
+std::vector<std::array<double, 3>> pose_coordinates(const LigandInstance& in, const Genotype& g) {
+  check_genotype(in, g, "pose_coordinates");
+  FlatInstance fi(in);
+  const std::vector<double> gv = flat_genotypes({g});
+  std::vector<double> xyz(3 * in.atoms.size());
+  check(mdr_pose_coords_batch(ctx(), &fi.c, gv.data(), 1, xyz.data()));
+  std::vector<std::array<double, 3>> out(in.atoms.size());
+  for (std::size_t i = 0; i < out.size(); ++i) out[i] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+  return out;
+}
+
+Clustering cluster_poses(const LigandInstance& in, const std::vector<Genotype>& poses,
+                         const std::vector<double>& energies, double tol) {
+  if (energies.size() != poses.size()) throw SizeError("cluster_poses needs one energy per pose");
+  for (const Genotype& g : poses) check_genotype(in, g, "cluster_poses");
+  FlatInstance fi(in);
+  const std::vector<double> gv = flat_genotypes(poses);
+  Clustering c;
+  c.cluster_of.resize(poses.size());
+  c.rmsd_to_seed.resize(poses.size());
+  int32_t nc = 0;
+  check(mdr_cluster_poses(ctx(), &fi.c, gv.data(), energies.data(), static_cast<int>(poses.size()), tol,
+                          reinterpret_cast<int32_t*>(c.cluster_of.data()), c.rmsd_to_seed.data(), &nc));
+  c.n_clusters = nc;
+  return c;
+}
+
+// ---------------------------------------------------------------- screen
+std::vector<ScreenResult> screen_batch(const Receptor& rec, const std::vector<LigandInstance>& ligs,
+                                       const std::vector<LigandChemistry>& chem, int runs, ReduceMethod method,
+                                       const LgaSettings& settings, const std::vector<std::uint64_t>& seeds,
+                                       double tol) {
+  if (chem.size() != ligs.size()) throw SizeError("screen_batch needs chemistry per ligand");
+  if (seeds.size() != ligs.size() * static_cast<std::size_t>(runs)) throw SizeError("one seed per (ligand, run)");
+  std::vector<std::unique_ptr<FlatInstance>> fis;
+  std::vector<std::unique_ptr<FlatChem>> fcs;
+  std::vector<mdr_instance> ci;
+  std::vector<mdr_ligand_params> cp;
+  std::size_t gtot = 0;
+  for (std::size_t j = 0; j < ligs.size(); ++j) {
+    fis.push_back(std::make_unique<FlatInstance>(ligs[j]));
+    fcs.push_back(std::make_unique<FlatChem>(ligs[j], chem[j]));
+    ci.push_back(fis.back()->c);
+    cp.push_back(fcs.back()->c);
+    gtot += static_cast<std::size_t>(runs) * (6 + ligs[j].n_rot);
+  }
+  const std::size_t R = seeds.size();
+  const mdr_lga_settings cs = to_c(settings);
+  std::vector<double> be(R), bg(gtot), rm(R);
+  std::vector<int64_t> ev(R);
+  std::vector<int32_t> cv(R), cl(R), nc(ligs.size());
+  check(mdr_grid_screen_batch(ctx(), dev_grid(rec), ci.data(), cp.data(), static_cast<int>(ligs.size()), runs,
+                              method_id(method), &cs, seeds.data(), tol, be.data(), bg.data(), ev.data(), cv.data(),
+                              cl.data(), rm.data(), nc.data()));
+  std::vector<ScreenResult> out(ligs.size());
+  std::size_t o = 0;
+  for (std::size_t j = 0; j < ligs.size(); ++j) {
+    ScreenResult& r = out[j];
+    const int dim = 6 + ligs[j].n_rot;
+    for (int k = 0; k < runs; ++k, o += static_cast<std::size_t>(dim)) {
+      const std::size_t i = j * static_cast<std::size_t>(runs) + static_cast<std::size_t>(k);
+      r.best_energy.push_back(be[i]);
+      r.best_genotype.push_back(make_genotype(bg.data() + o, ligs[j].n_rot));
+      r.evaluations.push_back(ev[i]);
+      r.converged.push_back(cv[i] != 0);
+      r.clusters.cluster_of.push_back(cl[i]);
+      r.clusters.rmsd_to_seed.push_back(rm[i]);
+    }
+    r.clusters.n_clusters = nc[j];
+  }
+  return out;
+}
+
 }  // namespace b200
 
 ScoreResult score(const LigandInstance& in, const Genotype& g, ReduceMethod method, AccumMode accum, int partition) {

@@ -260,6 +260,62 @@ static void docking_scenarios() {
   CHECK(gold.best_energy == -10.292128562927246 && gold.evaluations == 27572 && gold.runs.size() == 181);
 }
 
+// Extensions (mdreduce::b200): grid-map scoring, clustering, screening.
+static void extensions() {
+  const LigandInstance s3 = load("s3.mdri");
+  b200::GridShape shape;
+  shape.nx = shape.ny = shape.nz = 33;
+  shape.n_types = 2;
+  shape.origin = {-6.0, -6.0, -6.0};
+  shape.spacing = 0.375;
+  b200::ReceptorFields f;
+  for (std::size_t j = 0; j < s3.sites.size(); ++j) {
+    f.site_charge.push_back(0.1 * static_cast<double>(j) - 0.15);
+    f.site_volume.push_back(1.0);
+  }
+  f.type_depth_scale = {1.0, 0.7};
+  f.type_dist_scale = {1.0, 1.1};
+  const b200::Receptor rec = b200::Receptor::build(s3, f, shape);
+  const b200::GridMaps maps = rec.download();
+  CHECK(maps.maps.size() == 4u * 33 * 33 * 33);
+  const b200::Receptor rec2 = b200::Receptor::upload(maps);  // round trip
+  b200::LigandChemistry ch;
+  for (std::size_t i = 0; i < s3.atoms.size(); ++i) {
+    ch.atom_type.push_back(static_cast<int>(i % 2));
+    ch.charge.push_back(i % 3 == 0 ? 0.2 : -0.1);
+    ch.radius.push_back(0.45);
+    ch.epsilon.push_back(0.05);
+  }
+  Genotype g;
+  g.torsions.assign(static_cast<std::size_t>(s3.n_rot), 0.3);
+  g.x = 0.4;
+  g.phi = 0.2;
+  const auto a = b200::grid_score_batch(rec, s3, ch, {g}, ReduceMethod::Baseline, 64);
+  const auto b = b200::grid_score_batch(rec2, s3, ch, {g}, ReduceMethod::TcuSplit, 64);
+  CHECK(a.size() == 1 && std::isfinite(a[0].energy) && a[0].gradient.size() == 14u);
+  CHECK(std::abs(a[0].energy - b[0].energy) <= 1e-5f * std::max(1.0f, std::abs(a[0].energy)));
+  CHECK_THROWS_AS(b200::grid_score_batch(rec, s3, ch, {g}, ReduceMethod::Baseline, 16), UnsupportedBlockSizeError);
+  LgaSettings st;
+  st.generations = 2;
+  const auto runs = b200::grid_lga_run_batch(rec, s3, ch, ReduceMethod::Baseline, st, {1, 2, 3, 4});
+  CHECK(runs.size() == 4 && runs[0].evaluations > 0 && runs[0].best_energy <= runs[0].runs.back().best_energy);
+  std::vector<Genotype> poses;
+  std::vector<double> energies;
+  for (const DockResult& r : runs) {
+    poses.push_back(r.best_genotype);
+    energies.push_back(r.best_energy);
+  }
+  const b200::Clustering c = b200::cluster_poses(s3, poses, energies, 2.0);
+  CHECK(c.n_clusters >= 1 && c.n_clusters <= 4 && c.cluster_of.size() == 4u);
+  const auto xyz = b200::pose_coordinates(s3, poses[0]);
+  CHECK(xyz.size() == s3.atoms.size());
+  const auto scr = b200::screen_batch(rec, {s3, s3}, {ch, ch}, 4, ReduceMethod::Baseline, st,
+                                      {1, 2, 3, 4, 1, 2, 3, 4}, 2.0);
+  CHECK(scr.size() == 2 && scr[0].best_energy == scr[1].best_energy);
+  for (int k = 0; k < 4; ++k) CHECK(scr[0].best_energy[static_cast<std::size_t>(k)] == runs[static_cast<std::size_t>(k)].best_energy);
+  CHECK(scr[0].clusters.cluster_of == c.cluster_of && scr[0].clusters.n_clusters == c.n_clusters);
+}
+
 int main(int argc, char** argv) {
   if (argc < 2) {
     std::printf("usage: %s <data dir>\n", argv[0]);
@@ -267,7 +323,8 @@ int main(int argc, char** argv) {
   }
   g_data = argv[1];
   const std::pair<const char*, std::function<void()>> suites[] = {
-      {"half", half_frozen}, {"mma", mma_frozen}, {"reduce", reduce_frozen}, {"docking", docking_scenarios}};
+      {"half", half_frozen}, {"mma", mma_frozen}, {"reduce", reduce_frozen}, {"docking", docking_scenarios},
+      {"extensions", extensions}};
   for (const auto& [name, fn] : suites) {
     const int before = g_fail;
     fn();
