@@ -281,14 +281,18 @@ __device__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, boo
       const int ga = S.tors[a];
       const float4 pa = S.pos[a], ca = S.chem[a];
       float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f;
+      // branch-free: a same-group partner (incl. j == a) contributes with
+      // weight 0 instead of a divergent `continue`; its u is offset by 1 so
+      // the masked terms stay finite even for zero radii
+#pragma unroll 4
       for (int j = u % C; j < S.na; j += C) {
         const int gj = S.tors[j];
-        if (gj == ga) continue;
         const float4 pj = S.pos[j], cj = S.chem[j];
         const float dx = pa.x - pj.x, dy = pa.y - pj.y, dz = pa.z - pj.z;
         const float d0 = ca.x + cj.x;
         const float d02 = d0 * d0;
-        const float u2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, 0.5625f * d02)));
+        const float on = gj == ga ? 0.0f : 1.0f;
+        const float u2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, fmaf(0.5625f, d02, 1.0f - on))));
         float iu;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iu) : "f"(u2));
         const float rho2 = 1.5625f * d02 * iu;
@@ -297,8 +301,8 @@ __device__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, boo
         const float eps = ca.y * cj.y;
         const float qq = ca.w * cj.z;
         const float e = fmaf(eps, fmaf(-2.0f, rho6, rho12), qq * iu);
-        const float s = fmaf(-12.0f * eps, rho12 - rho6, -2.0f * qq * iu) * iu;
-        ee = fmaf(gj < 0 ? 1.0f : 0.5f, e, ee);
+        const float s = on * (fmaf(-12.0f * eps, rho12 - rho6, -2.0f * qq * iu) * iu);
+        ee = fmaf(gj == ga ? 0.0f : (gj < 0 ? 1.0f : 0.5f), e, ee);
         fx = fmaf(s, dx, fx);
         fy = fmaf(s, dy, fy);
         fz = fmaf(s, dz, fz);
@@ -312,19 +316,19 @@ __device__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, boo
     if (lane < 7) S.wpart[warp * 8 + lane] = w;
   }
   __syncthreads();  // S3
-  // D: totals in warp order, gradient component tid
-  float sums[7];
-#pragma unroll
-  for (int c = 0; c < 7; ++c) {
+  // D: totals in warp order (each thread reads only the components it
+  // needs: the energy, plus force / torque for gradient entries 0..5)
+  auto total = [&](int c) {
     float s = 0.f;
     for (int w = 0; w < S.W; ++w) s += S.wpart[w * 8 + c];
-    sums[c] = s;
-  }
-  out.e = sums[0];
+    return s;
+  };
+  out.e = total(0);
   if (tid < dim) {
     if (tid < 3) {
-      out.gd = sums[1 + tid];
+      out.gd = total(1 + tid);
     } else if (tid < 6) {
+      const float sums[7] = {0.f, 0.f, 0.f, 0.f, total(4), total(5), total(6)};
       d3 ax;
       if (tid == 3)
         ax = {0.0, 0.0, 1.0};
