@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
-              f"-I{INCLUDE}", f"-I{CSRC}"]
+              f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("MDR_NVCC_EXTRA", "").split()  # experiments only
     objs, procs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
