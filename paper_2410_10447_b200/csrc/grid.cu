@@ -221,7 +221,7 @@ struct GridEval {
 };
 
 template <int METHOD>
-__device__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, bool intra, bool bad_in, bool& bad_out) {
+__device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, bool intra, bool bad_in, bool& bad_out) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nr = S.nr, dim = 6 + nr;
   // A: angles owned by threads 3..dim-1
@@ -375,7 +375,7 @@ struct GridLs {
 // 16-deep best history is a per-warp register ring (slot = iter mod 16).
 // On return S.best holds the best genotype (after a barrier).
 template <int METHOD>
-__device__ GridLs grid_local_search(const GridSmem& S, const GridView& G, bool intra, const double* start,
+__device__ __forceinline__ GridLs grid_local_search(const GridSmem& S, const GridView& G, bool intra, const double* start,
                                     int max_iters, double tol) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int dim = 6 + S.nr;
