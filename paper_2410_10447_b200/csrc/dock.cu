@@ -433,20 +433,6 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
   if (lane == 0) D.pope[0][(size_t)run * D.P + p] = (double)o.sums[0];
 }
 
-__global__ void lga_init_finalize(LgaDev D) {
-  const int run = blockIdx.x * blockDim.x + threadIdx.x;
-  if (run >= D.R) return;
-  D.best_e[run] = 1.7976931348623157e308;  // numeric_limits<double>::max()
-  for (int d = 0; d < D.dim; ++d) D.best_g[(size_t)run * D.dim + d] = 0.0;
-  for (int p = 0; p < D.P; ++p)
-    track_best(D, run, D.pop[0] + ((size_t)run * D.P + p) * D.dim, D.pope[0][(size_t)run * D.P + p]);
-  D.evals[run] = D.P;
-  D.cur[run] = 0;
-  D.nrec[run] = 0;
-  D.conv[run] = 0;
-  D.status[run] = MDR_OK;
-  D.active[run] = D.gens > 0 && budget_ok(D, D.P);
-}
 
 // One offspring per warp: elitism, two binary tournaments, per-dimension
 // arithmetic crossover, Gaussian mutation, angle normalisation, score
@@ -559,29 +545,102 @@ __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
   }
 }
 
-// Sequential bookkeeping of one generation, in the reference's order:
-// track_best over offspring 1..off, then LS write-back / track / record in
-// rank order; swap populations; budget test for the next generation.
+// First occurrence of the strict minimum of candidate energies e(0..n-1)
+// (NaN never wins), by the calling warp: the result of applying
+// track_best (docking.cpp:408-413) to the candidates in order, starting from
+// `cur`.  Returns -1 when no candidate is below `cur`.
+template <class E>
+__device__ __forceinline__ int warp_first_min(int n, double cur, E&& energy) {
+  const int lane = threadIdx.x & 31;
+  double m = cur;
+  int idx = -1;
+  for (int k = lane; k < n; k += 32) {
+    const double e = energy(k);
+    if (e < m) {  // per lane, k ascending: first occurrence kept
+      m = e;
+      idx = k;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const double om = __shfl_xor_sync(kFull, m, off);
+    const int oi = __shfl_xor_sync(kFull, idx, off);
+    if (oi >= 0 && (idx < 0 || om < m || (om == m && oi < idx))) {
+      m = om;
+      idx = oi;
+    }
+  }
+  return idx;
+}
+
+// Initial population bookkeeping (docking.cpp:405-422), warp per run:
+// track_best over the P scored individuals in index order.
+__global__ void lga_init_finalize(LgaDev D) {
+  const int lane = threadIdx.x & 31;
+  const int run = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (run >= D.R) return;
+  const double* pe = D.pope[0] + (size_t)run * D.P;
+  const int w = warp_first_min(D.P, 1.7976931348623157e308, [&](int p) { return pe[p]; });
+  const double* g = D.pop[0] + ((size_t)run * D.P + (w < 0 ? 0 : w)) * D.dim;
+  for (int d = lane; d < D.dim; d += 32) D.best_g[(size_t)run * D.dim + d] = w < 0 ? 0.0 : g[d];
+  if (lane == 0) {
+    D.best_e[run] = w < 0 ? 1.7976931348623157e308 : pe[w];  // numeric_limits<double>::max()
+    D.evals[run] = D.P;
+    D.cur[run] = 0;
+    D.nrec[run] = 0;
+    D.conv[run] = 0;
+    D.status[run] = MDR_OK;
+    D.active[run] = D.gens > 0 && budget_ok(D, D.P);
+  }
+}
+
+// Bookkeeping of one generation, warp per run, with the reference's
+// sequential semantics (docking.cpp:472-496): track_best over offspring
+// 1..off, then for each LS rank r: write back, track_best, record.  The
+// sequential best tracking is the first occurrence of the minimum over that
+// candidate order; write-backs go to distinct offspring and run in parallel.
 __global__ void lga_gen_finalize(LgaDev D, int gen) {
-  const int run = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int run = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (run >= D.R || !D.active[run]) return;
   const int c = D.cur[run];
   double* nxt = D.pop[c ^ 1] + (size_t)run * D.P * D.dim;
   double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
-  for (int i = 1; i <= D.off; ++i) track_best(D, run, nxt + (size_t)i * D.dim, ne[i]);
-  long long evals = D.evals[run] + D.off;
-  for (int r = 0; r < D.L; ++r) {
-    const size_t o = (size_t)run * D.L + r;
-    const int t = D.lstarget[o];
-    for (int d = 0; d < D.dim; ++d) nxt[(size_t)t * D.dim + d] = D.lsg[o * D.dim + d];
-    ne[t] = D.lse[o];
-    evals += D.lsit[o] + 1;
-    track_best(D, run, D.lsg + o * D.dim, D.lse[o]);
-    push_record(D, run, D.lse[o], D.lsit[o], D.lscv[o]);
+  const size_t o0 = (size_t)run * D.L;
+  const int n = D.off + D.L;
+  const int w = warp_first_min(n, D.best_e[run], [&](int k) { return k < D.off ? ne[1 + k] : D.lse[o0 + k - D.off]; });
+  if (w >= 0) {  // copy the winner before any write-back overwrites it
+    const double* g = w < D.off ? nxt + (size_t)(1 + w) * D.dim : D.lsg + (o0 + w - D.off) * D.dim;
+    for (int d = lane; d < D.dim; d += 32) D.best_g[(size_t)run * D.dim + d] = g[d];
+    if (lane == 0) D.best_e[run] = w < D.off ? ne[1 + w] : D.lse[o0 + w - D.off];
   }
-  D.evals[run] = evals;
-  D.cur[run] = c ^ 1;
-  D.active[run] = (gen + 1 < D.gens) && D.status[run] == MDR_OK && budget_ok(D, evals);
+  __syncwarp();
+  long long it = 0;
+  for (int r = lane; r < D.L; r += 32) it += D.lsit[o0 + r] + 1;
+  for (int q = lane; q < D.L * D.dim; q += 32) {
+    const int r = q / D.dim, d = q % D.dim;
+    nxt[(size_t)D.lstarget[o0 + r] * D.dim + d] = D.lsg[(o0 + r) * D.dim + d];
+  }
+  const int k0 = D.nrec[run];
+  for (int r = lane; r < D.L; r += 32) {
+    ne[D.lstarget[o0 + r]] = D.lse[o0 + r];
+    if (k0 + r < D.maxrec) {
+      mdr_ls_record rec;
+      rec.best_energy = D.lse[o0 + r];
+      rec.iterations = D.lsit[o0 + r];
+      rec.converged = D.lscv[o0 + r];
+      D.recs[(size_t)run * D.maxrec + k0 + r] = rec;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) it += __shfl_xor_sync(kFull, it, off);
+  if (lane == 0) {
+    const long long evals = D.evals[run] + D.off + it;
+    D.nrec[run] = k0 + D.L;
+    D.evals[run] = evals;
+    D.cur[run] = c ^ 1;
+    D.active[run] = (gen + 1 < D.gens) && D.status[run] == MDR_OK && budget_ok(D, evals);
+  }
 }
 
 // Final polish from the incumbent best (docking.cpp:501-515), warp per run.
@@ -759,16 +818,28 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
   return cudaGetLastError();
 }
 
+// Warps of the CTA-per-pose final polish in the fast pair modes (the polish
+// runs one search per LGA run, so its latency, not throughput, counts).
+#ifndef MDR_POLISH_CTA
+#define MDR_POLISH_CTA 4  // measured: 0 / 2 / 4 / 8 -> 139.3 / 139.4 / 141.3 / 141.3 M evals/s on C3
+#endif
+static int polish_warps(int pair, int cta_warps) {
+  return cta_warps > 0 ? cta_warps : (pair != MDR_PAIR_FP64 ? MDR_POLISH_CTA : 0);
+}
+
 cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps) {
   const size_t smem = warp_smem(L, wpb);
+  const int pw = polish_warps(pair, cta_warps);
   cudaError_t e = prep_lga_init_kernel(method, pair, smem);
   if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, smem);
   if (cta_warps > 0) {
-    const size_t cs = cta_smem(L, cta_warps);
-    if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cs);
-    if (e == cudaSuccess) e = prep_lga_polish_cta_kernel(method, pair, cs);
+    if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
   } else {
     if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, smem);
+  }
+  if (pw > 0) {
+    if (e == cudaSuccess) e = prep_lga_polish_cta_kernel(method, pair, cta_smem(L, pw));
+  } else {
     if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, smem);
   }
   return e;
@@ -786,7 +857,7 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
   int launches = 0;
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 2], s);
   dispatch_lga_init_kernel(method, pair, blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s, L, D);
-  lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
+  lga_init_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D);
   launches += 2;
   for (int gen = 0; gen < D.gens; ++gen) {
     dispatch_lga_offspring_kernel(method, pair, blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s, L, D,
@@ -799,12 +870,13 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
         dispatch_lga_ls_kernel(method, pair, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
     }
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
-    lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
+    lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
     launches += D.L > 0 ? 3 : 2;
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
-  if (cta_warps > 0)
-    dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * cta_warps, cs, s, L, D);
+  const int pw = polish_warps(pair, cta_warps);
+  if (pw > 0)
+    dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * pw, cta_smem(L, pw), s, L, D);
   else
     dispatch_lga_polish_kernel(method, pair, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
@@ -815,12 +887,12 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
 }
 
 cudaError_t launch_lga_init_finalize(const LgaDev& D, cudaStream_t s) {
-  lga_init_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D);
+  lga_init_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lga_gen_finalize(const LgaDev& D, int gen, cudaStream_t s) {
-  lga_gen_finalize<<<(D.R + 127) / 128, 128, 0, s>>>(D, gen);
+  lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
   return cudaGetLastError();
 }
 
