@@ -584,10 +584,82 @@ def c5_measure(torch, local, n_ligands=256, runs=10, method="baseline", batch=25
     return out
 
 
+def score_throughput(lib, torch, local, n=1 << 20, reps=5):
+    """Raw score+gradient kernel throughput at full occupancy: n independent
+    random C3 poses (analytic, FP64-fast) and C4 poses (grid mode) per launch,
+    device resident, CUDA events, L2 flushed before each launch.  This is the
+    K3 kernel alone (no search), so it fills the GPU unlike a 100-run docking."""
+    from paper_2410_10447_b200 import Device
+    from paper_2410_10447_b200.workloads import c4
+
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    out = {}
+    dev = Device(local)
+    dev.set_stream(stream.cuda_stream)
+
+    def timed(call):
+        call()
+        torch.cuda.synchronize()
+        ms = []
+        for k in range(reps):
+            flush.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            call()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        return statistics.median(ms)
+
+    gen = torch.Generator(device=f"cuda:{local}").manual_seed(7)
+    for name, (inst, grid_case) in {"c3_analytic": (workload(), None), "c4_grid": (None, c4())}.items():
+        if grid_case is None:
+            di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+            dg = None
+            part, method = 64, BASELINE
+        else:
+            inst, params, fields, grid, settings = grid_case
+            dg = lib.mdr_grid_build(dev.ctx, inst.cref(), fields.cref(), grid.cref())
+            di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+            assert lib.mdr_instance_set_grid(dev.ctx, di, dg, params.cref()) == 0
+            part, method = 128, BASELINE
+        m = n if grid_case is None else n // 4
+        g = torch.empty((m, inst.dim), dtype=torch.float64, device=f"cuda:{local}")
+        g[:, :3].uniform_(-3.0, 3.0, generator=gen)
+        g[:, 3:].uniform_(-math.pi, math.pi, generator=gen)
+        e = torch.empty(m, dtype=torch.float32, device=f"cuda:{local}")
+        gr = torch.empty((m, inst.dim), dtype=torch.float32, device=f"cuda:{local}")
+        tq = torch.empty((m, 3), dtype=torch.float32, device=f"cuda:{local}")
+
+        def call():
+            rc = lib.mdr_score_dev(dev.ctx, di, C.c_void_p(g.data_ptr()), m, method, SINGLE, part,
+                                   C.c_void_p(e.data_ptr()), C.c_void_p(gr.data_ptr()), C.c_void_p(tq.data_ptr()))
+            assert rc == 0, lib.mdr_last_error(dev.ctx)
+
+        ms = timed(call)
+        rec = {"poses_per_launch": m, "ms_per_launch": ms, "evals_per_s": m / (ms * 1e-3)}
+        if grid_case is None:
+            fl = flop_per_eval(inst, part)
+            rec.update({"flop_per_eval": fl, "fp64_TFLOPs": fl * m / (ms * 1e-3) / 1e12,
+                        "fp64_frac_of_peak": fl * m / (ms * 1e-3) / 1e12 / fp64_peak_tflops(torch)})
+        else:
+            fl, nb, _ = grid_flop_bytes_per_eval(inst, params, part)
+            rec.update({"flop_per_eval": fl, "map_bytes_per_eval": nb, "fp32_TFLOPs": fl * m / (ms * 1e-3) / 1e12,
+                        "map_GBps": nb * m / (ms * 1e-3) / 1e9})
+        out[name] = rec
+        lib.mdr_instance_free(dev.ctx, di)
+        if dg:
+            lib.mdr_grid_free(dev.ctx, dg)
+    dev.close()
+    return out
+
+
 def extra_measurements(args, dev, lib, torch):
     """Mode sweep of the docking step, C4 grid-mode docking, C2 reduction
     microbench (ns/call)."""
     out = {"modes": mode_sweep(lib, torch, torch.cuda.current_device(), workload(), LgaSettings())}
+    out["score_kernel"] = score_throughput(lib, torch, torch.cuda.current_device())
     out["c4_grid"] = c4_measure(lib, torch, torch.cuda.current_device())
     out["c5_screen"] = c5_measure(torch, torch.cuda.current_device())
     if hasattr(lib, "mdr_reduce_bench_dev"):

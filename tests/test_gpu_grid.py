@@ -158,3 +158,33 @@ def test_grid_errors_before_work(dev, small):
     bad = LigandParams(np.full(inst.n_atoms, 9), lp.charge, lp.radius, lp.epsilon)
     with pytest.raises(SizeError):
         dev.grid_score_batch(dg, inst, bad, poses, BASELINE, 64)
+
+
+def test_c4_full_size_maps_and_scores(port, dev):
+    """BASELINE config C4 at full size: 126^3 x 6 maps built on the device
+    (48 MB) equal the oracle's builder at sampled lattice points (oracle run
+    on 2x2x2 sub-lattices anchored there), and the 100-atom / 30-torsion
+    ligand scores on those maps match the oracle scoring the downloaded maps."""
+    from paper_2410_10447_b200._abi import Grid
+    from paper_2410_10447_b200.workloads import c4
+
+    inst, params, fields, grid, _ = c4()
+    dg = dev.grid_build(inst, fields, grid)
+    maps = dg.download()
+    assert maps.shape == (6, 126, 126, 126)
+    rng = derive_rng(3, "c4/points")
+    for _ in range(12):
+        ix, iy, iz = (int(rng.next_index(125)) for _ in range(3))
+        sub = Grid((2, 2, 2), grid.n_types, tuple(o + grid.spacing * i for o, i in zip(grid.origin, (ix, iy, iz))),
+                   grid.spacing)
+        want = port.grid_build(inst, fields, sub)
+        got = maps[:, iz:iz + 2, iy:iy + 2, ix:ix + 2]
+        ulp = np.abs(got.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
+        assert ulp.max() <= 2
+    G = Grid(grid.shape, grid.n_types, grid.origin, grid.spacing, maps)
+    poses = _poses(inst, 12, 9, spread=4.0)
+    e, g, _ = dev.grid_score_batch(dg, inst, params, poses, BASELINE, 128)
+    for i, p in enumerate(poses):
+        we, wg, _, _ = port.grid_score(inst, G, params, p)
+        assert abs(e[i] - we) <= 1e-5 * max(1.0, abs(we))
+        assert np.abs(g[i] - wg).max() <= 2e-5 * max(1.0, np.abs(wg).max())
