@@ -357,6 +357,30 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* grid, const mdr_inst
                           double* best_energy, double* best_genotype, int64_t* evaluations, int32_t* converged,
                           int32_t* cluster_of, double* rmsd_to_seed, int32_t* n_clusters);
 
+/* ---- native multi-GPU host driver (north_star subsystem 4, SURVEY §8 e) --
+ * One host thread + one context per listed device (a device may be listed
+ * more than once).  No collective: every thread writes its results at the
+ * run / ligand's own offsets of the caller's arrays (the final gather).
+ * Results equal a single-device call with the same seeds. */
+/* LGA runs sharded statically (run i -> devices[i % n_devices]); outputs as
+ * mdr_lga_run_batch (best_genotype n_runs x dim). */
+int mdr_multi_lga_run_batch(const int* devices, int n_devices, const mdr_instance* inst, int method, int accum,
+                            int pair_precision, const mdr_lga_settings* settings, const uint64_t* seeds, int n_runs,
+                            double* best_energy, double* best_genotype, int64_t* evaluations, int32_t* converged);
+/* Virtual screen over the node: every device builds the receptor maps once,
+ * then pulls batches of batch_ligands ligands from a shared atomic queue
+ * (dynamic balancing of unequal ligand costs) and docks each batch with
+ * mdr_grid_screen_batch.  Outputs as mdr_grid_screen_batch over all ligands;
+ * device_of_ligand[j] = index into `devices` of the device that docked j. */
+int mdr_multi_screen(const int* devices, int n_devices, const mdr_instance* receptor_sites,
+                     const mdr_receptor_fields* fields, const mdr_grid* shape, const mdr_instance* ligands,
+                     const mdr_ligand_params* params, int n_ligands, int runs_per_ligand, int method,
+                     const mdr_lga_settings* settings, const uint64_t* seeds, double rmsd_tol, int batch_ligands,
+                     double* best_energy, double* best_genotype, int64_t* evaluations, int32_t* cluster_of,
+                     int32_t* n_clusters, int32_t* device_of_ligand);
+/* Message of the last failing multi-device call on this thread. */
+const char* mdr_multi_last_error(void);
+
 /* ---- RMSD clustering of docked poses ----------------------
  * Not in the reference.  Poses become world coordinates through
  * evaluate_atoms' transform (docking.cpp:101-106, FP64); clustering is

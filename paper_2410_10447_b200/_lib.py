@@ -71,6 +71,9 @@ _SIGS = {
     "mdr_grid_lga_run_batch": (I, [P, P, P, P, I, P, P, I, P, P, P, P, P, P]),
     "mdr_pose_coords_batch": (I, [P, P, P, I, P]),
     "mdr_grid_screen_batch": (I, [P, P, P, P, I, I, I, P, P, D, P, P, P, P, P, P, P]),
+    "mdr_multi_lga_run_batch": (I, [P, I, P, I, I, I, P, P, I, P, P, P, P]),
+    "mdr_multi_screen": (I, [P, I, P, P, P, P, P, I, I, I, P, P, D, I, P, P, P, P, P, P]),
+    "mdr_multi_last_error": (C.c_char_p, []),
     "mdr_cluster_poses": (I, [P, P, P, P, I, D, P, P, P]),
     "mdr_cluster_segments_dev": (I, [P, P, P, P, P, I, I, D, P, P, P]),
     "mdr_lga_batch_cluster": (I, [P, P, D, P, P, P]),

@@ -432,6 +432,50 @@ class DevGrid:
             pass
 
 
+def multi_lga_run_batch(devices, inst: Instance, method, accum, settings: LgaSettings, seeds,
+                        pair: int = PAIR_FP64_FAST):
+    """Native multi-GPU docking (mdr_multi_lga_run_batch): runs sharded
+    round-robin over `devices`, one host thread + context per device.
+    Returns (best_energy[n], best_genotype[n, dim], evaluations[n], converged[n])."""
+    lib = _lib.load()
+    dv = np.ascontiguousarray(devices, np.int32)
+    seeds = np.ascontiguousarray(seeds, np.uint64).reshape(-1)
+    n = seeds.size
+    be, bg = np.zeros(n), np.zeros((n, inst.dim))
+    ev, cv = np.zeros(n, np.int64), np.zeros(n, np.int32)
+    rc = lib.mdr_multi_lga_run_batch(_p(dv), dv.size, inst.cref(), method, accum, pair, C.byref(settings), _p(seeds), n,
+                                     _p(be), _p(bg), _p(ev), _p(cv))
+    raise_for(rc, lib.mdr_multi_last_error().decode())
+    return be, bg, ev, cv.astype(bool)
+
+
+def multi_screen(devices, sites: Instance, fields: ReceptorFields, grid: Grid, ligands, params, runs_per_ligand: int,
+                 method, settings: LgaSettings, seeds, rmsd_tol: float = 2.0, batch_ligands: int = 256):
+    """Native multi-GPU virtual screen (mdr_multi_screen): each device builds
+    the receptor once and pulls ligand batches from a shared queue.  Returns
+    (best_energy[n*R], best_genotype packed, evaluations[n*R],
+    cluster_of[n*R], n_clusters[n], device_of_ligand[n])."""
+    from ._abi import CInstance, CLigandParams
+
+    lib = _lib.load()
+    dv = np.ascontiguousarray(devices, np.int32)
+    n, R = len(ligands), runs_per_ligand
+    seeds = np.ascontiguousarray(seeds, np.uint64).reshape(-1)
+    ci = (CInstance * n)(*[l.c() for l in ligands])
+    cp = (CLigandParams * n)(*[p.c() for p in params])
+    be = np.zeros(n * R)
+    bg = np.zeros(sum(R * l.dim for l in ligands))
+    ev = np.zeros(n * R, np.int64)
+    cl = np.zeros(n * R, np.int32)
+    nc = np.zeros(n, np.int32)
+    dol = np.full(n, -1, np.int32)
+    rc = lib.mdr_multi_screen(_p(dv), dv.size, sites.cref(), fields.cref(), grid.cref(), ci, cp, n, R, method,
+                              C.byref(settings), _p(seeds), rmsd_tol, batch_ligands, _p(be), _p(bg), _p(ev), _p(cl),
+                              _p(nc), _p(dol))
+    raise_for(rc, lib.mdr_multi_last_error().decode())
+    return be, bg, ev, cl, nc, dol
+
+
 @dataclass
 class MethodSummary:
     min: float

@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libmdr_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU = ["reduce.cu", "dock.cu", "grid.cu", "cluster.cu", "bench_reduce.cu", "tc05_reduce.cu"]
-CPP = ["capi.cpp", "dropin.cpp"]
+CPP = ["capi.cpp", "dropin.cpp", "multi.cpp"]
 
 
 def sources():
@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}:\n{out}")
         if verbose and out:
             print(out)
-    link = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", LIB, *objs,
+    link = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-Xcompiler", "-pthread", "-o", LIB, *objs,
             "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     p = subprocess.run(link, capture_output=True, text=True)
     if p.returncode != 0:
