@@ -81,7 +81,6 @@ __global__ void cluster_kernel(const double* __restrict__ xyz, long long xstride
     ord[r] = p;
   }
   __shared__ int s_hit, s_nc;
-  __shared__ double s_r;
   if (threadIdx.x == 0) s_nc = 0;
   __syncthreads();
   for (int q = 0; q < n; ++q) {
