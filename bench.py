@@ -489,7 +489,7 @@ def grid_flop_bytes_per_eval(inst, params, partition):
     return 80 * inst.n_atoms + (30 * pairs if params.intra else 0), 96 * inst.n_atoms, pairs
 
 
-def c4_measure(lib, torch, local, methods=("baseline", "split", "tcu"), partitions=(128,), steps=3, runs=N_RUNS):
+def c4_measure(lib, torch, local, methods=("baseline", "split", "tcu"), partitions=(64, 128), steps=3, runs=N_RUNS):
     """C4 (BASELINE.json configs[3]) on this GPU: 100-atom / 30-torsion
     ligand, grid mode on 126^3 maps, `runs` LGA runs, device resident, events
     on the launching stream, L2 flushed before every step."""
@@ -623,7 +623,7 @@ def score_throughput(lib, torch, local, n=1 << 20, reps=5):
             dg = lib.mdr_grid_build(dev.ctx, inst.cref(), fields.cref(), grid.cref())
             di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
             assert lib.mdr_instance_set_grid(dev.ctx, di, dg, params.cref()) == 0
-            part, method = 128, BASELINE
+            part, method = settings.partition, BASELINE
         m = n if grid_case is None else n // 4
         g = torch.empty((m, inst.dim), dtype=torch.float64, device=f"cuda:{local}")
         g[:, :3].uniform_(-3.0, 3.0, generator=gen)

@@ -38,7 +38,7 @@ struct GridSmem {
   int* grp_off;     // nr + 1
   int* grp_atoms;   // nta
   double2* trig[2]; // (3 + nr) x (sin, cos), double buffered
-  float4* pos;      // na: R * local (lever arm), FP32
+  float4* pos;      // na: R * local (lever arm), FP32; w = torsion group (int bits)
   float4* force;    // na: grid force
   float4* fintra;   // nta * C: intramolecular force partials
   float* wpart;     // W x 8
@@ -259,7 +259,7 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
     float3 F;
     const float e = grid_atom(G, S.type[i], (float)at.w, ch.z, tx + r.x, ty + r.y, tz + r.z, F);
     const float3 rf = make_float3((float)r.x, (float)r.y, (float)r.z);
-    S.pos[i] = make_float4(rf.x, rf.y, rf.z, 0.f);
+    S.pos[i] = make_float4(rf.x, rf.y, rf.z, __int_as_float(k));
     S.force[i] = make_float4(F.x, F.y, F.z, 0.f);
     const float3 tq = cross3f(rf, F);
     rec[0] += e;
@@ -286,8 +286,8 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
       // the masked terms stay finite even for zero radii
 #pragma unroll 4
       for (int j = u % C; j < S.na; j += C) {
-        const int gj = S.tors[j];
         const float4 pj = S.pos[j], cj = S.chem[j];
+        const int gj = __float_as_int(pj.w);
         const float dx = pa.x - pj.x, dy = pa.y - pj.y, dz = pa.z - pj.z;
         const float d0 = ca.x + cj.x;
         const float d02 = d0 * d0;

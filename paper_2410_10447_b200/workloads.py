@@ -45,7 +45,7 @@ def c4():
     inst.name = "synth/large"
     params = random_ligand_params(derive_rng(SEED, "synth/large/chem"), inst.n_atoms, N_TYPES)
     _, fields, grid = c4_receptor()
-    return inst, params, fields, grid, LgaSettings(partition=128)
+    return inst, params, fields, grid, LgaSettings(partition=64)  # 64 measured faster than 128 (profiles/r1_c4_probe.json)
 
 
 def c5_ligand(j: int, receptor_sites):
