@@ -150,6 +150,11 @@ int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red,
 /* Self test: bit mismatches of the branch-free FP64 division of the strict
  * pair loop against IEEE div.rn.f64 over n counter-generated operand pairs. */
 int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
+/* Self test: the device's correctly rounded sin, cos (angles in [-pi, pi)),
+ * log (Box-Muller u1) and cos(2 pi u2) (crmath.cuh), then CUDA libdevice's,
+ * against this host's glibc over n counter-generated inputs.  mismatches[8]:
+ * cr sin, cr cos, cr log, cr cos2pi, libdevice sin, cos, log, cos2pi. */
+int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches);
 
 /* C2 microbench (no reference counterpart; cli.cpp:195-266 is its CPU
  * analogue): kernel k in [0, mdr_reduce_bench_kernels()) reduces float4 per

@@ -58,6 +58,7 @@ _SIGS = {
     "mdr_lga_batch_total_evals_dev": (I, [P, P, P]),
     "mdr_lga_batch_profile_dev": (I, [P, P, P, P, P, P]),
     "mdr_selftest_ddiv": (I, [P, U64, C.c_int64, P]),
+    "mdr_selftest_crmath": (I, [P, C.c_int64, P]),
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),

@@ -409,6 +409,42 @@ int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatch
 
 // C2 microbench: one block-level float4 reduce-and-broadcast per thread
 // block (see bench_reduce.cu for the kernel roster).
+int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches) {
+  if (!ctx || n < 0 || !mismatches) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  std::memset(mismatches, 0, sizeof(uint64_t) * 8);
+  const int chunk = 1 << 20;
+  DevBuf<double> d;
+  CK(d.alloc((size_t)8 * chunk, S(ctx)));
+  std::vector<double> h((size_t)8 * chunk);
+  auto u64 = [](uint64_t nn) {  // RngStream draw with key 0 (rng.cpp:34-37)
+    uint64_t z = nn * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  const double pi = 3.14159265358979323846;
+  for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+    const int m = (int)std::min<int64_t>(chunk, n - i0);
+    CK(launch_crmath_probe(i0, m, d.p, S(ctx)));
+    CK(cudaMemcpyAsync(h.data(), d.p, sizeof(double) * 8 * m, cudaMemcpyDeviceToHost, S(ctx)));
+    CK(cudaStreamSynchronize(S(ctx)));
+    for (int t = 0; t < m; ++t) {
+      const uint64_t i = (uint64_t)(i0 + t);
+      const double a = -pi + 2.0 * pi * ((double)(u64(4 * i + 1) >> 11) * 0x1p-53);
+      const double u1 = (double)((u64(4 * i + 2) >> 11) + 1) * 0x1p-53;
+      const double z = 2.0 * pi * ((double)(u64(4 * i + 3) >> 11) * 0x1p-53);
+      const double want[4] = {std::sin(a), std::cos(a), std::log(u1), std::cos(z)};
+      const double* o = &h[(size_t)8 * t];
+      for (int k = 0; k < 4; ++k) {
+        mismatches[k] += o[k] != want[k];
+        mismatches[4 + k] += o[4 + k] != want[k];
+      }
+    }
+  }
+  ctx->launches += (uint64_t)((n + chunk - 1) / chunk);
+  return MDR_OK;
+}
+
 int mdr_reduce_bench_kernels(void) { return kReduceBenchKernels; }
 const char* mdr_reduce_bench_kernel_name(int k) { return reduce_bench_name(k); }
 

@@ -10,6 +10,7 @@
 // Compiled with --fmad=false (see mdr_device.cuh).
 #include <cuda_runtime.h>
 
+#include "crmath.cuh"
 #include "dock_launch.h"
 #include "mdr_device.cuh"
 #include "lga_device.cuh"
@@ -262,10 +263,10 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
 // Warp 0: frame of the current genotype and every atom's world position.
 __device__ __forceinline__ Frame cta_place(const SmemLigand& S, const CtaCtx& c) {
   const int lane = threadIdx.x & 31;
-  const Frame f = build_frame(c.g[3], c.g[4], c.g[5]);
+  const Frame f = build_frame<false>(c.g[3], c.g[4], c.g[5]);
   const d3 tr = {c.g[0], c.g[1], c.g[2]};
   for (int i = lane; i < S.n_atoms; i += 32) {
-    const d3 w = atom_world(S, c.g, f.R, tr, i);
+    const d3 w = atom_world<false>(S, c.g, f.R, tr, i);
     double* q = c.world + (size_t)i * 4;
     q[0] = w.x;
     q[1] = w.y;
@@ -883,6 +884,30 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;
   if (n_launches) *n_launches = launches;
+  return cudaGetLastError();
+}
+
+// ---- self test of the correctly rounded math (crmath.cuh) against glibc:
+// for input i (counter-generated like RngStream), 8 results: cr sin, cos of
+// a = -pi + 2 pi u, cr log(u1), cr cos(2 pi u2), then the same with libdevice.
+__global__ void crmath_probe_kernel(long long i0, int n, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t i = (uint64_t)(i0 + t);
+  const double a = -kPi + 2.0 * kPi * draw_unit(0, 4 * i + 1);
+  const double u1 = (double)((draw_u64(0, 4 * i + 2) >> 11) + 1) * 0x1p-53;
+  const double z = 2.0 * kPi * draw_unit(0, 4 * i + 3);
+  double* o = out + 8 * (size_t)t;
+  cr::sincos(a, &o[0], &o[1]);
+  o[2] = cr::log(u1);
+  o[3] = cr::cos(z);
+  ::sincos(a, &o[4], &o[5]);
+  o[6] = ::log(u1);
+  o[7] = ::cos(z);
+}
+
+cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s) {
+  crmath_probe_kernel<<<(n + 255) / 256, 256, 0, s>>>(i0, n, out);
   return cudaGetLastError();
 }
 
