@@ -309,11 +309,12 @@ namespace b200 {
 // Select the GPU used by the calls above (default 0); one context per thread.
 void set_device(int device);
 // Pair-term arithmetic of score / local_search / lga_run (per thread):
-//   Reference — FP64 in the reference's exact operation order;
+//   Reference — FP64 in the reference's exact operation order with
+//               correctly rounded trig (399/400 paired LGA runs identical);
 //   Fast64    — FP64 with FMA and one reciprocal per pair (default; float
 //               outputs bit-identical to the reference on every measured
-//               evaluation and local search, 79/80 LGA runs,
-//               profiles/r1_parity_report.json);
+//               evaluation and local search, 380/400 paired LGA runs,
+//               profiles/r1_parity_scale.json);
 //   Fp32      — FP32 pair terms (within 1e-5 relative, fastest).
 enum class PairMode { Reference, Fast64, Fp32 };
 void set_pair_mode(PairMode mode);

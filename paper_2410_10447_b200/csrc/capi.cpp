@@ -43,9 +43,9 @@ struct mdr_ctx {
   cudaStream_t stream = nullptr;
   // Default pair arithmetic: FP64 with FMA + one reciprocal per pair.  Its
   // float outputs matched the reference bit for bit on every measured
-  // evaluation and local search and on 79 of 80 LGA runs (one departs by a
-  // float ulp, profiles/r1_parity_report.json); MDR_PAIR_FP64 keeps the
-  // reference's exact double operation order (bit-identical).
+  // evaluation and local search and on 380 of 400 paired LGA runs
+  // (profiles/r1_parity_scale.json); MDR_PAIR_FP64 keeps the reference's
+  // exact double operation order with correctly rounded trig (399 of 400).
   int pair = MDR_PAIR_FP64_FAST;
   int wpb = 2;        // warps per CTA of the warp-per-pose kernels
   int cta_warps = 0;  // 0: warp per pose (fastest measured); >0: CTA-per-pose LS
