@@ -160,14 +160,39 @@ std::pair<std::array<float, 7>, SyncStats> reduce7(std::span<const Partial7> rec
                                                    AccumMode accum_mode);
 
 // ---------------------------------------------------------------- simblock
-// simblock.hpp:10-19 (block-shape validation only; the abstract cost model
-// is replaced by ncu measurements)
+// simblock.hpp:10-65.  The reductions run on the GPU; the abstract cost
+// model (estimate_cost / scaling_sweep) is kept for API compatibility and
+// evaluates the same model counters the reference does (real device
+// behaviour: ncu, profiles/).
 struct BlockConfig {
   BlockConfig(int threads, ReduceMethod m, AccumMode a);
   int threads_per_block;
   ReduceMethod method;
   AccumMode accum_mode;
 };
+struct CostWeights {
+  double block_sync = 10.0;
+  double atomic = 4.0;
+  double shuffle = 1.0;
+  double fence = 4.0;
+  double mma = 8.0;
+};
+// One block of cfg.threads_per_block records through the configured method.
+std::pair<Vec4, SyncStats> simulate_block(const BlockConfig& cfg, std::span<const Vec4> values);
+std::pair<std::array<float, 7>, SyncStats> simulate_block(const BlockConfig& cfg, std::span<const Partial7> values);
+double estimate_cost(const SyncStats& stats, const CostWeights& weights);
+struct SweepRow {
+  int threads_per_block = 0;
+  SyncStats baseline;
+  SyncStats tcu;
+  double cost_baseline = 0.0;
+  double cost_tcu = 0.0;
+  double cost_ratio = 0.0;  // baseline / tcu
+  bool degenerate = false;  // tcu cost 0: ratio reported as 1.0
+};
+std::vector<SweepRow> scaling_sweep(std::span<const int> sizes, const CostWeights& weights,
+                                    AccumMode accum_mode = AccumMode::Half);
+inline constexpr std::array<int, 5> kDefaultSweepSizes = {64, 128, 256, 512, 1024};
 
 // ---------------------------------------------------------------- rng
 // rng.hpp:10-43 (pure uint64 arithmetic; host side)
@@ -206,6 +231,24 @@ struct LigandInstance {
 };
 LigandInstance parse_instance(std::string_view text);
 std::string serialize_instance(const LigandInstance& instance);
+// One docking-run record of the results CSV (instance_io.hpp:52-65).
+struct ResultRow {
+  std::uint64_t seed = 0;
+  std::string method;      // "baseline" | "tcu"
+  std::string accum_mode;  // "half" | "single"
+  std::string instance;
+  double best_energy = 0.0;
+  std::int64_t evaluations = 0;
+  bool converged = false;
+  std::uint64_t block_syncs = 0;
+  std::uint64_t atomic_adds = 0;
+  std::uint64_t mma_ops = 0;
+  friend bool operator==(const ResultRow&, const ResultRow&) = default;
+};
+// RFC-4180-style CSV with the fixed header row, %.17g numbers
+// (instance_io.hpp:67-73); parse_results throws ParseError(line).
+std::string write_results(std::span<const ResultRow> rows);
+std::vector<ResultRow> parse_results(std::string_view csv);
 
 // ---------------------------------------------------------------- docking
 // docking.hpp:17-169

@@ -4,6 +4,8 @@
 // API surface (Genotype accessors, BlockConfig, RngStream, MDRI parsing)
 // is restated here from the reference's documented behaviour.
 #include <algorithm>
+#include <charconv>
+#include <cstdio>
 #include <bit>
 #include <cmath>
 #include <cstring>
@@ -254,6 +256,55 @@ BlockConfig::BlockConfig(int threads, ReduceMethod m, AccumMode a)  // simblock.
                                     std::to_string(threads));
 }
 
+// One block through the configured method (simblock.cpp:21-58): Tcu ->
+// reduce4; Baseline -> one baseline block reduction per component (a single
+// device launch of mdr_reduce4_batch with method BASELINE).
+std::pair<Vec4, SyncStats> simulate_block(const BlockConfig& cfg, std::span<const Vec4> values) {
+  if (values.size() != static_cast<std::size_t>(cfg.threads_per_block))
+    throw SizeError("simulate_block got " + std::to_string(values.size()) + " records for " +
+                    std::to_string(cfg.threads_per_block) + " threads");
+  if (cfg.method == ReduceMethod::Tcu) return reduce4(values, cfg.accum_mode);
+  float out[4];
+  mdr_sync_stats st;
+  check(mdr_reduce4_batch(ctx(), reinterpret_cast<const float*>(values.data()), static_cast<int>(values.size()), 1,
+                          method_id(cfg.method), accum_id(cfg.accum_mode), out, &st));
+  return {Vec4{out[0], out[1], out[2], out[3]}, to_stats(st)};
+}
+
+std::pair<std::array<float, 7>, SyncStats> simulate_block(const BlockConfig& cfg, std::span<const Partial7> values) {
+  if (values.size() != static_cast<std::size_t>(cfg.threads_per_block))
+    throw SizeError("simulate_block got " + std::to_string(values.size()) + " records for " +
+                    std::to_string(cfg.threads_per_block) + " threads");
+  return reduce7(values, cfg.method, cfg.accum_mode);
+}
+
+double estimate_cost(const SyncStats& st, const CostWeights& w) {  // simblock.cpp:60-66
+  return static_cast<double>(st.block_syncs) * w.block_sync + static_cast<double>(st.atomic_adds) * w.atomic +
+         static_cast<double>(st.warp_shuffles) * w.shuffle + static_cast<double>(st.memory_fences) * w.fence +
+         static_cast<double>(st.mma_ops) * w.mma;
+}
+
+// Counter profile of one baseline block reduction vs one tcu reduce4 per
+// block size (simblock.cpp:68-98), both obtained from the device calls.
+std::vector<SweepRow> scaling_sweep(std::span<const int> sizes, const CostWeights& w, AccumMode accum) {
+  std::vector<SweepRow> rows;
+  for (const int n : sizes) {
+    const BlockConfig tcu_cfg(n, ReduceMethod::Tcu, accum), base_cfg(n, ReduceMethod::Baseline, accum);
+    (void)tcu_cfg;
+    (void)base_cfg;
+    SweepRow row;
+    row.threads_per_block = n;
+    row.baseline = baseline_block_reduce(std::vector<float>(static_cast<std::size_t>(n), 0.0f), n).second;
+    row.tcu = reduce4(std::vector<Vec4>(static_cast<std::size_t>(n)), accum).second;
+    row.cost_baseline = estimate_cost(row.baseline, w);
+    row.cost_tcu = estimate_cost(row.tcu, w);
+    row.degenerate = row.cost_tcu == 0.0;
+    row.cost_ratio = row.degenerate ? 1.0 : row.cost_baseline / row.cost_tcu;
+    rows.push_back(row);
+  }
+  return rows;
+}
+
 // ---------------------------------------------------------------- rng
 namespace {
 std::uint64_t mix64(std::uint64_t z) {
@@ -380,6 +431,112 @@ std::string serialize_instance(const LigandInstance& in) {
     o << "site " << s.pos[0] << ' ' << s.pos[1] << ' ' << s.pos[2] << ' ' << s.depth << ' ' << s.preferred_distance
       << '\n';
   return o.str();
+}
+
+// ---------------------------------------------------------------- results CSV
+namespace {
+constexpr std::string_view kResultHeader =
+    "seed,method,accum_mode,instance,best_energy,evaluations,converged,block_syncs,atomic_adds,mma_ops";
+
+std::string csv_text(std::string_view s) {  // quoted only when needed, "" escapes
+  if (s.find_first_of(",\"\n") == std::string_view::npos) return std::string(s);
+  std::string q = "\"";
+  for (const char c : s) q += c == '"' ? std::string("\"\"") : std::string(1, c);
+  return q + "\"";
+}
+
+std::string num17(double v) {
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+
+template <class T>
+T parse_num(const std::string& f, int line, const char* what) {
+  T v{};
+  const auto [p, ec] = std::from_chars(f.data(), f.data() + f.size(), v);
+  if (ec != std::errc() || p != f.data() + f.size())
+    throw ParseError(line, std::string("bad ") + what + " '" + f + "'");
+  return v;
+}
+}  // namespace
+
+std::string write_results(std::span<const ResultRow> rows) {
+  std::string out(kResultHeader);
+  out += '\n';
+  for (const ResultRow& r : rows)
+    out += std::to_string(r.seed) + ',' + csv_text(r.method) + ',' + csv_text(r.accum_mode) + ',' +
+           csv_text(r.instance) + ',' + num17(r.best_energy) + ',' + std::to_string(r.evaluations) + ',' +
+           (r.converged ? "true" : "false") + ',' + std::to_string(r.block_syncs) + ',' +
+           std::to_string(r.atomic_adds) + ',' + std::to_string(r.mma_ops) + '\n';
+  return out;
+}
+
+std::vector<ResultRow> parse_results(std::string_view csv) {
+  std::vector<ResultRow> rows;
+  bool header = false;
+  int line = 0;
+  std::size_t pos = 0;
+  while (pos < csv.size()) {
+    // one record: up to the first newline outside quotes (quoted fields may
+    // span lines; errors name the record's first line)
+    const int first = ++line;
+    std::vector<std::string> f(1);
+    bool quoted = false, any = false;
+    for (; pos < csv.size(); ++pos) {
+      const char c = csv[pos];
+      if (quoted) {
+        if (c == '"') {
+          if (pos + 1 < csv.size() && csv[pos + 1] == '"') {
+            f.back() += '"';
+            ++pos;
+          } else {
+            quoted = false;
+          }
+        } else {
+          if (c == '\n') ++line;
+          f.back() += c;
+        }
+      } else if (c == '"') {
+        if (!f.back().empty()) throw ParseError(first, "unexpected quote inside unquoted field");
+        quoted = any = true;
+      } else if (c == ',') {
+        f.emplace_back();
+        any = true;
+      } else if (c == '\n') {
+        ++pos;
+        break;
+      } else {
+        f.back() += c;
+        any = true;
+      }
+    }
+    if (quoted) throw ParseError(first, "unterminated quoted field");
+    if (!any) continue;  // empty line
+    if (!header) {
+      std::string joined;
+      for (std::size_t i = 0; i < f.size(); ++i) joined += (i ? "," : "") + f[i];
+      if (joined != kResultHeader) throw ParseError(first, "unexpected results header");
+      header = true;
+      continue;
+    }
+    if (f.size() != 10) throw ParseError(first, "expected 10 fields, got " + std::to_string(f.size()));
+    ResultRow r;
+    r.seed = parse_num<std::uint64_t>(f[0], first, "seed");
+    r.method = f[1];
+    r.accum_mode = f[2];
+    r.instance = f[3];
+    r.best_energy = parse_num<double>(f[4], first, "best_energy");
+    r.evaluations = parse_num<std::int64_t>(f[5], first, "evaluations");
+    if (f[6] != "true" && f[6] != "false") throw ParseError(first, "bad converged flag '" + f[6] + "'");
+    r.converged = f[6] == "true";
+    r.block_syncs = parse_num<std::uint64_t>(f[7], first, "block_syncs");
+    r.atomic_adds = parse_num<std::uint64_t>(f[8], first, "atomic_adds");
+    r.mma_ops = parse_num<std::uint64_t>(f[9], first, "mma_ops");
+    rows.push_back(std::move(r));
+  }
+  if (!header) throw ParseError(1, "missing results header");
+  return rows;
 }
 
 // ---------------------------------------------------------------- docking

@@ -260,6 +260,41 @@ static void docking_scenarios() {
   CHECK(gold.best_energy == -10.292128562927246 && gold.evaluations == 27572 && gold.runs.size() == 181);
 }
 
+// simblock / instance_io surface (test_simblock.cpp, test_cli.cpp:163-164,
+// test_rng_io.cpp CSV cases).
+static void simblock_and_csv() {
+  const auto rows = scaling_sweep(kDefaultSweepSizes, CostWeights{}, AccumMode::Half);
+  const double want[5] = {10.1666667, 15.7727273, 22.5, 28.9347826, 33.8846154};
+  CHECK(rows.size() == 5);
+  for (int i = 0; i < 5; ++i) CHECK(std::abs(rows[static_cast<std::size_t>(i)].cost_ratio - want[i]) < 1e-6);
+  std::vector<Vec4> v(128);
+  for (int i = 0; i < 128; ++i) v[static_cast<std::size_t>(i)] = {float(i % 5), 1.0f, float(i % 3) - 1.0f, 0.5f};
+  const auto t = simulate_block(BlockConfig(128, ReduceMethod::Tcu, AccumMode::Single), v);
+  const auto d = reduce4(v, AccumMode::Single);
+  CHECK(t.first.x == d.first.x && t.first.e == d.first.e && t.second == d.second);
+  const auto b = simulate_block(BlockConfig(128, ReduceMethod::Baseline, AccumMode::Single), v);
+  std::vector<float> xs(128);
+  for (int i = 0; i < 128; ++i) xs[static_cast<std::size_t>(i)] = v[static_cast<std::size_t>(i)].x;
+  CHECK(b.first.x == baseline_block_reduce(xs, 128).first && b.second.block_syncs == 12);
+  CHECK_THROWS_AS(simulate_block(BlockConfig(64, ReduceMethod::Tcu, AccumMode::Half), v), SizeError);
+  CHECK(estimate_cost(b.second, CostWeights{}) > 0.0);
+  ResultRow r;
+  r.seed = 7;
+  r.method = "baseline";
+  r.accum_mode = "single";
+  r.instance = "s1, \"quoted\"";
+  r.best_energy = -10.296875;
+  r.evaluations = 25549;
+  r.converged = true;
+  r.block_syncs = 21;
+  const std::vector<ResultRow> rr = {r, r};
+  const std::string csv = write_results(rr);
+  CHECK(csv.rfind("seed,method,accum_mode,instance,best_energy,evaluations,converged,block_syncs,atomic_adds,mma_ops\n", 0) == 0);
+  CHECK(csv.find("7,baseline,single,\"s1, \"\"quoted\"\"\",-10.296875,25549,true,21,0,0\n") != std::string::npos);
+  CHECK(parse_results(csv) == rr);
+  CHECK_THROWS_AS(parse_results("bogus\n"), ParseError);
+}
+
 // Extensions (mdreduce::b200): grid-map scoring, clustering, screening.
 static void extensions() {
   const LigandInstance s3 = load("s3.mdri");
@@ -324,7 +359,7 @@ int main(int argc, char** argv) {
   g_data = argv[1];
   const std::pair<const char*, std::function<void()>> suites[] = {
       {"half", half_frozen}, {"mma", mma_frozen}, {"reduce", reduce_frozen}, {"docking", docking_scenarios},
-      {"extensions", extensions}};
+      {"simblock+csv", simblock_and_csv}, {"extensions", extensions}};
   for (const auto& [name, fn] : suites) {
     const int before = g_fail;
     fn();
