@@ -375,7 +375,9 @@ int mdr_multi_lga_run_batch(const int* devices, int n_devices, const mdr_instanc
 /* Virtual screen over the node: every device builds the receptor maps once,
  * then pulls batches of batch_ligands ligands from a shared atomic queue
  * (dynamic balancing of unequal ligand costs) and docks each batch with
- * mdr_grid_screen_batch.  Outputs as mdr_grid_screen_batch over all ligands;
+ * mdr_grid_screen_batch.  A device that fails (device error) retires and
+ * its batch goes back to the queue for the others; the call fails only if
+ * no device is left or a batch is invalid.  Outputs as mdr_grid_screen_batch over all ligands;
  * device_of_ligand[j] = index into `devices` of the device that docked j. */
 int mdr_multi_screen(const int* devices, int n_devices, const mdr_instance* receptor_sites,
                      const mdr_receptor_fields* fields, const mdr_grid* shape, const mdr_instance* ligands,
@@ -385,6 +387,10 @@ int mdr_multi_screen(const int* devices, int n_devices, const mdr_instance* rece
                      int32_t* n_clusters, int32_t* device_of_ligand);
 /* Message of the last failing multi-device call on this thread. */
 const char* mdr_multi_last_error(void);
+/* Test hook (SURVEY §5 fault injection): make device index `device_index`
+ * of the next mdr_multi_screen calls fail on its `batch`-th batch (-1: off).
+ * A failed device retires and its batch is re-queued to the others. */
+void mdr_multi_set_fault_injection(int device_index, int batch);
 
 /* ---- RMSD clustering of docked poses ----------------------
  * Not in the reference.  Poses become world coordinates through

@@ -75,6 +75,7 @@ _SIGS = {
     "mdr_multi_lga_run_batch": (I, [P, I, P, I, I, I, P, P, I, P, P, P, P]),
     "mdr_multi_screen": (I, [P, I, P, P, P, P, P, I, I, I, P, P, D, I, P, P, P, P, P, P]),
     "mdr_multi_last_error": (C.c_char_p, []),
+    "mdr_multi_set_fault_injection": (None, [I, I]),
     "mdr_cluster_poses": (I, [P, P, P, P, I, D, P, P, P]),
     "mdr_cluster_segments_dev": (I, [P, P, P, P, P, I, I, D, P, P, P]),
     "mdr_lga_batch_cluster": (I, [P, P, D, P, P, P]),

@@ -7,13 +7,19 @@
 //  * mdr_multi_screen: ligands pulled from a shared atomic work queue in
 //    batches (ligand costs differ by ~100x, so a dynamic queue balances the
 //    devices), each batch one mdr_grid_screen_batch launch sequence against
-//    the device's own copy of the receptor maps.
+//    the device's own copy of the receptor maps.  Failure handling (SURVEY
+//    §5): a device whose batch fails with a device error retires and puts
+//    the batch on a retry list that the surviving devices drain; the call
+//    fails only if every device has retired (or on a non-device error, e.g.
+//    a ligand the path rejects).  mdr_multi_set_fault_injection(d, k) makes
+//    device index d fail on its k-th batch (tests).
 // The only exchange is the final gather: every thread writes its results
 // into the caller's arrays at the run / ligand's own offsets (no collective,
 // no NCCL: the path is embarrassingly parallel).  Results are identical to a
 // single-device call on the same seeds (tests/test_multi.py).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -30,6 +36,8 @@ struct CtxGuard {
     if (c) mdr_ctx_destroy(c);
   }
 };
+
+std::atomic<int> g_fault_device{-1}, g_fault_batch{0};
 
 struct FirstError {  // the first failure of any device thread wins
   std::mutex m;
@@ -56,6 +64,11 @@ int finish(FirstError& fe) {
 extern "C" {
 
 const char* mdr_multi_last_error(void) { return t_multi_err.c_str(); }
+
+void mdr_multi_set_fault_injection(int device_index, int batch) {
+  g_fault_device.store(device_index);
+  g_fault_batch.store(batch);
+}
 
 int mdr_multi_lga_run_batch(const int* devices, int n_devices, const mdr_instance* inst, int method, int accum,
                             int pair_precision, const mdr_lga_settings* s, const uint64_t* seeds, int n_runs,
@@ -111,30 +124,71 @@ int mdr_multi_screen(const int* devices, int n_devices, const mdr_instance* rece
   // genotype offsets of each ligand in the packed best_genotype output
   std::vector<size_t> goff(n_ligands + 1, 0);
   for (int j = 0; j < n_ligands; ++j) goff[j + 1] = goff[j] + (size_t)R * (6 + ligands[j].n_rot);
-  std::atomic<int> next{0};
+  // Work queue: fresh batches in order, then batches handed back by retired
+  // devices.  A device leaves only when nothing is queued and no batch is in
+  // flight anywhere (an in-flight batch may still come back).
+  std::mutex qm;
+  int next_j = 0, busy = 0;
+  std::vector<int> retry;
   FirstError fe;
+  auto acquire = [&]() -> int {
+    for (;;) {
+      {
+        std::lock_guard<std::mutex> g(qm);
+        if (fe.rc != MDR_OK) return -1;
+        if (next_j < n_ligands) {
+          const int j = next_j;
+          next_j += batch_ligands;
+          ++busy;
+          return j;
+        }
+        if (!retry.empty()) {
+          const int j = retry.back();
+          retry.pop_back();
+          ++busy;
+          return j;
+        }
+        if (busy == 0) return -1;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  };
+  auto release = [&](int handed_back) {
+    std::lock_guard<std::mutex> g(qm);
+    if (handed_back >= 0) retry.push_back(handed_back);
+    --busy;
+  };
   std::vector<std::thread> pool;
   for (int t = 0; t < n_devices; ++t) {
     pool.emplace_back([&, t] {
       CtxGuard g;
       g.c = mdr_ctx_create(devices[t]);
-      if (!g.c) return fe.set(MDR_ERR_CUDA, "mdr_ctx_create failed");
+      if (!g.c) return;  // this device never takes work
       mdr_dev_grid* dg = mdr_grid_build(g.c, receptor_sites, fields, shape);  // receptor once per device
-      if (!dg) return fe.set(MDR_ERR_CUDA, mdr_last_error(g.c));
+      if (!dg) return;
+      int done = 0;
       for (;;) {
-        const int j0 = next.fetch_add(batch_ligands);
-        if (j0 >= n_ligands || fe.rc != MDR_OK) break;
+        const int j0 = acquire();
+        if (j0 < 0) break;
         const int nb = std::min(batch_ligands, n_ligands - j0);
         std::vector<double> be((size_t)nb * R), bg(goff[j0 + nb] - goff[j0]);
         std::vector<int64_t> ev((size_t)nb * R);
         std::vector<int32_t> cl((size_t)nb * R), nc(nb), cv((size_t)nb * R);
-        const int rc = mdr_grid_screen_batch(g.c, dg, ligands + j0, params + j0, nb, R, method, s,
-                                             seeds + (size_t)j0 * R, rmsd_tol, be.data(), bg.data(), ev.data(),
-                                             cv.data(), cl.data(), nullptr, nc.data());
-        if (rc) {
-          fe.set(rc, mdr_last_error(g.c));
+        const int rc = (g_fault_device.load() == t && done == g_fault_batch.load())
+                           ? MDR_ERR_CUDA  // injected device failure
+                           : mdr_grid_screen_batch(g.c, dg, ligands + j0, params + j0, nb, R, method, s,
+                                                   seeds + (size_t)j0 * R, rmsd_tol, be.data(), bg.data(),
+                                                   ev.data(), cv.data(), cl.data(), nullptr, nc.data());
+        if (rc == MDR_ERR_CUDA) {  // device failure: hand the batch back and retire
+          release(j0);
           break;
         }
+        if (rc) {  // the batch itself is invalid: no device would succeed
+          fe.set(rc, mdr_last_error(g.c));
+          release(-1);
+          break;
+        }
+        ++done;
         const size_t r0 = (size_t)j0 * R;
         if (best_energy) std::memcpy(best_energy + r0, be.data(), sizeof(double) * be.size());
         if (best_genotype) std::memcpy(best_genotype + goff[j0], bg.data(), sizeof(double) * bg.size());
@@ -143,11 +197,14 @@ int mdr_multi_screen(const int* devices, int n_devices, const mdr_instance* rece
         if (n_clusters) std::memcpy(n_clusters + j0, nc.data(), sizeof(int32_t) * nb);
         if (device_of_ligand)
           for (int k = 0; k < nb; ++k) device_of_ligand[j0 + k] = t;
+        release(-1);
       }
       mdr_grid_free(g.c, dg);
     });
   }
   for (auto& th : pool) th.join();
+  if (fe.rc == MDR_OK && (!retry.empty() || next_j < n_ligands))
+    fe.set(MDR_ERR_CUDA, "every device failed; batches left undocked");
   return finish(fe);
 }
 

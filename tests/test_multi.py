@@ -42,3 +42,35 @@ def test_multi_screen_equals_single_device(dev):
     assert np.array_equal(cl, np.concatenate([r["cluster_of"] for r in ref]))
     assert np.array_equal(nc, [r["n_clusters"] for r in ref])
     assert np.array_equal(bg, np.concatenate([r["best_genotype"].ravel() for r in ref]))
+
+
+def test_multi_screen_requeues_a_failed_device(dev):
+    """Fault injection (SURVEY §5): device index 1 fails on its first batch;
+    its batch is re-queued, device 0 docks everything, results unchanged."""
+    from paper_2410_10447_b200 import _lib
+    from paper_2410_10447_b200.workloads import c4_receptor, c5_ligand
+
+    lib = _lib.load()
+    sites, fields, _ = c4_receptor()
+    grid = centered_grid(33, 0.375, 4)
+    ligs, params = zip(*[c5_ligand(j, sites) for j in range(8)])
+    s = LgaSettings(generations=1, partition=64)
+    seeds = np.arange(16, dtype=np.uint64) + 31
+    ref = multi_screen([0], sites, fields, grid, list(ligs), list(params), 2, BASELINE, s, seeds, 2.0,
+                       batch_ligands=2)
+    lib.mdr_multi_set_fault_injection(1, 0)
+    try:
+        got = multi_screen([0, 0], sites, fields, grid, list(ligs), list(params), 2, BASELINE, s, seeds, 2.0,
+                           batch_ligands=2)
+    finally:
+        lib.mdr_multi_set_fault_injection(-1, 0)
+    assert np.all(got[5] == 0)  # every ligand docked by the surviving device
+    for a, b in zip(ref[:5], got[:5]):
+        assert np.array_equal(a, b)
+    lib.mdr_multi_set_fault_injection(0, 0)
+    try:
+        with pytest.raises(Exception):  # the only device fails: the call fails
+            multi_screen([0], sites, fields, grid, list(ligs), list(params), 2, BASELINE, s, seeds, 2.0,
+                         batch_ligands=2)
+    finally:
+        lib.mdr_multi_set_fault_injection(-1, 0)
