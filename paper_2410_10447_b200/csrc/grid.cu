@@ -2,8 +2,8 @@
 // one CTA of `partition` threads evaluates one pose, AutoDock-GPU style.
 //
 // Per evaluation (three CTA barriers):
-//   A  threads 3..dim-1 take sincos of their own genotype angle (FP64)
-//      into a double-buffered table                              -> S1
+//   A  threads 3..dim-1 take sincos of their own genotype angle (FP32,
+//      widened) into a double-buffered table                      -> S1
 //   B  thread per atom: rotate_axis (docking.cpp:57-60), R*local + t
 //      (build_frame docking.cpp:78-91, FP64), trilinear interpolation of the
 //      atom's combined map w*type + q*elec + |q|*desolv (FP32, L1/L2-resident
@@ -25,6 +25,13 @@
 #include "dock_launch.h"
 #include "lga_device.cuh"
 #include "mdr_device.cuh"
+
+// Phase A trig in FP32: C4 43.7 -> 55.3 M evals/s (the other threads wait
+// at S1 for it), device-vs-oracle error 1.0e-6 -> 1.4e-6 (energy), 1.6e-6 ->
+// 1.1e-6 (gradient) (profiles/r1_grid_probe.json; tolerances 1e-5 / 2e-5).
+#ifndef MDR_GRID_F32_TRIG
+#define MDR_GRID_F32_TRIG 1
+#endif
 
 namespace mdr {
 
@@ -227,9 +234,15 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
   // A: angles owned by threads 3..dim-1
   double2* trig = S.trig[buf];
   if (tid >= 3 && tid < dim) {
+#if MDR_GRID_F32_TRIG
+    float s, c;  // FP32 trig (grid mode is tolerance parity; shortens the barrier wait)
+    sincosf((float)S.g[tid], &s, &c);
+    trig[tid - 3] = make_double2((double)s, (double)c);
+#else
     double s, c;
     sincos(S.g[tid], &s, &c);
     trig[tid - 3] = make_double2(s, c);
+#endif
   }
   bad_out = __syncthreads_or(bad_in) != 0;  // S1
   GridEval out;
