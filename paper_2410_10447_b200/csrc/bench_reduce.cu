@@ -349,7 +349,8 @@ __global__ void stream_kernel(const float4* __restrict__ in, int n_red, float4* 
 
 static const char* kNames[] = {"reducefs_x4 (AutoDock, K1a)", "shuffle_transpose (K1b)", "wmma_f16 (paper, K2)",
                                "split_tf32_block (K2p)", "split_tf32_warp (K2s)", "shuffle_2level (K1c)",
-                               "split_bf16x3_mma (K2b)", "tcgen05_batched_tf32x2 (K2t)"};
+                               "split_bf16x3_mma (K2b)", "tcgen05_batched_tf32x2 (K2t)",
+                               "tcgen05_tma_pipelined (K2t2)"};
 
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
                                 int blocks_per_sm, cudaStream_t s) {

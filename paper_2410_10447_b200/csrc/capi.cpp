@@ -455,9 +455,12 @@ int mdr_reduce_bench_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in,
   if (block < 64 || block > 1024 || block % 64)
     return fail(ctx, MDR_ERR_BLOCK_SIZE, "bench blocks are multiples of 64 in [64, 1024]");
   if (chain_steps > 0 && n_red % chain_steps) return fail(ctx, MDR_ERR_SIZE, "n_red must be a multiple of steps");
-  if (kernel == 7) {  // tcgen05 batched: streaming only (32 reductions per contraction)
-    if (chain_steps > 0) return fail(ctx, MDR_ERR_INVALID, "the tcgen05 batched kernel has no chain mode");
-    CK(launch_reduce4_tc05(d_in, block, n_red, d_out, 3, ctx->stream));
+  if (kernel == 7 || kernel == 8) {  // tcgen05 batched: streaming only (32 reductions per contraction)
+    if (chain_steps > 0) return fail(ctx, MDR_ERR_INVALID, "the tcgen05 batched kernels have no chain mode");
+    if (kernel == 7)
+      CK(launch_reduce4_tc05(d_in, block, n_red, d_out, 3, ctx->stream));
+    else
+      CK(launch_reduce4_tc05_tma(d_in, block, n_red, d_out, ctx->stream));
   } else {
     CK(launch_reduce_bench(kernel, block, d_in, n_red, chain_steps, d_out, 2048 / block, ctx->stream));
   }

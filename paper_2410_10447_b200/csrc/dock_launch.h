@@ -66,9 +66,11 @@ cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long*
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
                                 int blocks_per_sm, cudaStream_t s);
 const char* reduce_bench_name(int k);
-constexpr int kReduceBenchKernels = 8;  // id 7 = tcgen05 batched (stream mode only)
+constexpr int kReduceBenchKernels = 9;  // ids 7, 8 = tcgen05 batched (stream mode only; 8 = TMA-fed)
 
 // tc05_reduce.cu: batched float4 reductions, 32 per tcgen05 contraction
 cudaError_t launch_reduce4_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s);
+// K2t2: the same contraction fed by TMA bulk copies into a 6-deep ring
+cudaError_t launch_reduce4_tc05_tma(const float* in, int B, int n_red, float* out, cudaStream_t s);
 
 }  // namespace mdr

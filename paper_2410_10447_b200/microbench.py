@@ -97,7 +97,7 @@ def main():
     torch.cuda.set_stream(s)
     if args.kernel >= 0:
         for B in args.blocks:
-            if args.chain == 0 or args.kernel == 7:  # streaming mode
+            if args.chain == 0 or args.kernel in (7, 8):  # streaming mode
                 args.chain = 0
                 args.n = min(args.n, (4 << 30) // (16 * B))
             x = torch.rand((args.n // max(args.chain, 1), B, 4), device="cuda") * 2 - 1

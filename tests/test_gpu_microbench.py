@@ -9,7 +9,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 # max |err| / sum|x| per kernel (K2 = the paper's f16 accumulator)
-TOL = {0: 1e-6, 1: 1e-6, 2: 2e-2, 3: 1e-6, 4: 1e-6, 5: 1e-6, 6: 1e-6, 7: 1e-6}
+TOL = {0: 1e-6, 1: 1e-6, 2: 2e-2, 3: 1e-6, 4: 1e-6, 5: 1e-6, 6: 1e-6, 7: 1e-6, 8: 1e-6}
 
 
 @pytest.mark.parametrize("block", [64, 128, 256, 1024])
@@ -26,7 +26,7 @@ def test_microbench_kernels_sum_correctly(dev, block):
     want = x.double().sum(1)
     mass = x.double().abs().sum(1)
     for k in range(lib.mdr_reduce_bench_kernels()):
-        for steps in ((0,) if k == 7 else (0, 1)):  # streaming, and chain of length 1
+        for steps in ((0,) if k in (7, 8) else (0, 1)):  # streaming, and chain of length 1
             y.zero_()
             rc = lib.mdr_reduce_bench_dev(dev.ctx, k, block, C.c_void_p(x.data_ptr()), n, steps,
                                           C.c_void_p(y.data_ptr()))
