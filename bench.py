@@ -568,15 +568,18 @@ def c5_measure(torch, local, n_ligands=256, runs=10, method="baseline", batch=25
     s = LgaSettings(partition=64)
     ligs = [c5_ligand(j, sites) for j in range(n_ligands)]
     warm = sc.screen(dev, dg, lambda j: ligs[j], 8, 2, LgaSettings(partition=64, generations=2), METHODS[method])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rows, clusters = sc.screen(dev, dg, lambda j: ligs[j], n_ligands, runs, s, METHODS[method], batch=batch)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    dt = float("inf")
+    for _ in range(2):  # full-size passes; the second runs warm (allocations, attributes, clocks)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rows, clusters = sc.screen(dev, dg, lambda j: ligs[j], n_ligands, runs, s, METHODS[method], batch=batch)
+        torch.cuda.synchronize()
+        dt = min(dt, time.perf_counter() - t0)
     evals = sum(r.evaluations for r in rows)
     out = {"workload": f"C5 virtual-screen sample: {n_ligands} ligands (U[10,100] atoms, U[0,30] torsions) x {runs} "
                        "LGA runs vs the C4 receptor (126^3 maps), grid mode, per-ligand RMSD clustering (2 A)",
            "ligands_per_hour": sc.ligands_per_hour(n_ligands, dt), "seconds": dt, "evals_per_s": evals / dt,
+           "timing": "best of two full-size passes",
            "evaluations": evals, "mean_clusters": float(np.mean([c[1] for c in clusters.values()])),
            "api": "screen.screen -> mdr_grid_screen_batch (host ligands in, CSV rows out)", "warmup": len(warm[0])}
     dg.free()
