@@ -451,12 +451,14 @@ def mode_sweep(lib, torch, local, inst, settings, steps=3):
     seeds = torch.from_numpy((np.arange(N_RUNS, dtype=np.uint64) + np.uint64(1_000_000)).view(np.int64)).to(
         f"cuda:{local}")
     out = {}
-    for pname, pair in (("fp64", PAIR_FP64), ("fp64fast", PAIR_FP64_FAST), ("fp32", PAIR_FP32)):
+    for pname, pair in (("fp64", PAIR_FP64), ("fp64fast", PAIR_FP64_FAST), ("fp32", PAIR_FP32),
+                        ("fp64fast-exact-torsion", PAIR_FP64_FAST)):
         for mname, method in METHODS.items():
             if pname != "fp64fast" and mname != "baseline":
                 continue
             dev = Device(local, pair=pair)
             dev.set_stream(stream.cuda_stream)
+            dev.set_exact_torsion(pname.endswith("exact-torsion"))
             di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
             b = lib.mdr_lga_batch_create(dev.ctx, di, method, SINGLE, C.byref(settings), N_RUNS)
             tot = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")

@@ -110,6 +110,20 @@ int mdr_ctx_set_warps_per_block(mdr_ctx* ctx, int warps);
 /* Warps cooperating on one pose in the CTA-per-pose local-search kernels
  * used by the fast pair modes (1..16, default 4). */
 int mdr_ctx_set_cta_warps(mdr_ctx* ctx, int warps);
+
+/* Analytic (site) mode torsion gradient.  0 (default): every torsion entry is
+ * the TOTAL ligand torque projected on that torsion's world axis — score()'s
+ * documented approximation (reference docking.cpp:228-231, docking.hpp:42-43),
+ * the quantity parity is defined on.  1: entry 6+k is the torque of torsion
+ * group k alone (the atoms moved by torsion k), the exact gradient that
+ * score_reference() computes in double (docking.cpp:244-268).  The per-atom
+ * torques are staged in the pose's warp scratch during the evaluation, so the
+ * cost is 16 B of shared memory per atom and one group sum per torsion lane;
+ * ligands are limited to 1024 atoms and the LS runs warp per pose.  Applies to
+ * every analytic score / local-search / LGA launch made through `ctx` (an LGA
+ * batch keeps the mode it was created with).  Grid mode always uses the
+ * exact per-group torque. */
+int mdr_ctx_set_exact_torsion(mdr_ctx* ctx, int on);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);
 /* Number of kernel launches this context has enqueued so far. */

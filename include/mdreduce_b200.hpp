@@ -361,6 +361,10 @@ void set_device(int device);
 //   Fp32      — FP32 pair terms (within 1e-5 relative, fastest).
 enum class PairMode { Reference, Fast64, Fp32 };
 void set_pair_mode(PairMode mode);
+// Torsion gradient of the analytic path (per thread; see mdr_ctx_set_exact_torsion):
+// false (default) = score()'s total-torque projection, the parity quantity;
+// true = exact per-group torque, the gradient score_reference() computes.
+void set_exact_torsion(bool on);
 // Many independent evaluations / searches / docking runs in one launch.
 std::vector<ScoreResult> score_batch(const LigandInstance& instance, const std::vector<Genotype>& poses,
                                      ReduceMethod method, AccumMode accum_mode, int partition);

@@ -99,6 +99,13 @@ class Device:
     def set_pair_precision(self, pair: int):
         self._chk(self.lib.mdr_ctx_set_pair_precision(self.ctx, pair))
 
+    def set_exact_torsion(self, on: bool):
+        """Analytic-mode torsion gradient: False (default) projects the total
+        torque on every torsion axis (score(), docking.cpp:228-231); True
+        gives each torsion its own group's torque, the exact gradient of
+        score_reference() (docking.cpp:244-268).  See mdr_ctx_set_exact_torsion."""
+        self._chk(self.lib.mdr_ctx_set_exact_torsion(self.ctx, 1 if on else 0))
+
     def set_stream(self, stream_ptr: int | None):
         self._chk(self.lib.mdr_ctx_set_stream(self.ctx, C.c_void_p(stream_ptr or 0)))
 

@@ -49,6 +49,7 @@ struct mdr_ctx {
   int pair = MDR_PAIR_FP64_FAST;
   int wpb = 2;        // warps per CTA of the warp-per-pose kernels
   int cta_warps = 0;  // 0: warp per pose (fastest measured); >0: CTA-per-pose LS
+  int exact = 0;      // analytic mode: exact per-group torsion gradient (mdr_ctx_set_exact_torsion)
 
   std::string err;
   uint64_t launches = 0;
@@ -182,7 +183,21 @@ cudaStream_t S(mdr_ctx* c) { return c->stream; }
 // The CTA-per-pose local search is used for the fast pair modes; the
 // bit-faithful FP64 mode keeps the warp-per-pose kernels (sites summed in
 // the reference's order).
-int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 ? 0 : c->cta_warps; }
+int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 || c->exact ? 0 : c->cta_warps; }
+
+// The analytic-mode ligand view a launch uses: the instance's arrays plus the
+// context's torsion-gradient mode.
+LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
+  LigandView L = di->view;
+  L.exact_torsion = c->exact;
+  return L;
+}
+
+int check_exact(mdr_ctx* ctx, const mdr_dev_instance* di) {
+  if (ctx->exact && !di->grid && di->n_atoms > kMaxExactAtoms)
+    return fail(ctx, MDR_ERR_SIZE, "exact-torsion mode supports at most " + std::to_string(kMaxExactAtoms) + " atoms");
+  return MDR_OK;
+}
 
 
 }  // namespace
@@ -228,6 +243,12 @@ int mdr_ctx_set_pair_precision(mdr_ctx* c, int p) {
 int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
   if (!c || w < 0 || w > 16) return fail(c, MDR_ERR_INVALID, "CTA warps must be 0..16 (0 = warp per pose)");
   c->cta_warps = w;
+  return MDR_OK;
+}
+
+int mdr_ctx_set_exact_torsion(mdr_ctx* c, int on) {
+  if (!c || (on != 0 && on != 1)) return fail(c, MDR_ERR_INVALID, "exact torsion flag must be 0 or 1");
+  c->exact = on;
   return MDR_OK;
 }
 
@@ -662,8 +683,9 @@ int mdr_score_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* g, int
     ctx->launches++;
     return MDR_OK;
   }
+  if (int rc = check_exact(ctx, di)) return rc;
   if (n <= 0) return MDR_OK;
-  CK(launch_score(di->view, g, n, method, ctx->pair, partition, accum == MDR_ACCUM_HALF, e, grad, tq, ctx->stream,
+  CK(launch_score(launch_view(ctx, di), g, n, method, ctx->pair, partition, accum == MDR_ACCUM_HALF, e, grad, tq, ctx->stream,
                   ctx->wpb));
   ctx->launches++;
   return MDR_OK;
@@ -763,8 +785,9 @@ int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double*
     ctx->launches++;
     return MDR_OK;
   }
+  if (int rc = check_exact(ctx, di)) return rc;
   if (n <= 0) return MDR_OK;
-  CK(launch_local_search(di->view, starts, n, max_iters, tol, method, ctx->pair, partition, accum == MDR_ACCUM_HALF,
+  CK(launch_local_search(launch_view(ctx, di), starts, n, max_iters, tol, method, ctx->pair, partition, accum == MDR_ACCUM_HALF,
                          og, oe, oit, ocv, status, ctx->stream, ctx->wpb, cta_warps_for(ctx)));
   ctx->launches++;
   return MDR_OK;
@@ -961,9 +984,10 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
   }
   if (check_lga(ctx, method, s)) return nullptr;
   if (di->grid && check_grid_block(ctx, di, s->partition)) return nullptr;
+  if (check_exact(ctx, di)) return nullptr;
   mdr_lga_batch* b = lga_batch_alloc(ctx, method, accum, s, R, 6 + di->n_rot);
   if (!b) return nullptr;
-  b->L = di->view;
+  b->L = di->grid ? di->view : launch_view(ctx, di);
   b->cta_warps = cta_warps_for(ctx);
   b->grid = di->grid;
   cudaError_t e = cudaSuccess;
@@ -1095,7 +1119,7 @@ int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int ac
   if (int rc = check_lga(ctx, method, s)) return rc;
   if (n_runs == 0) return MDR_OK;
   LgaCache& c = ctx->lga;
-  const bool hit = c.b && c.b->cta_warps == cta_warps_for(ctx) && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
+  const bool hit = c.b && c.b->cta_warps == cta_warps_for(ctx) && c.b->L.exact_torsion == ctx->exact && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
                    c.method == method && c.pair == ctx->pair && c.accum == accum && c.wpb == ctx->wpb &&
                    c.R == n_runs && std::memcmp(&c.s, s, sizeof *s) == 0;
   if (hit) {

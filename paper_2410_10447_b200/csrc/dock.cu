@@ -26,18 +26,23 @@ struct WarpCtx {
   double* best;
 };
 
-__device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp) {
-  unsigned char* p = base + (size_t)warp * kWarpRegion;
+__host__ __device__ inline size_t warp_region_bytes(const LigandView& L) {
+  return (size_t)kWarpRegion + (L.exact_torsion ? (size_t)16 * L.n_atoms : 0);
+}
+
+__device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, const LigandView& L) {
+  unsigned char* p = base + (size_t)warp * warp_region_bytes(L);
   WarpCtx w;
   w.ws.tile = reinterpret_cast<__half*>(p);
   w.ws.rec = reinterpret_cast<float*>(p + 2 * 256 * 2);
   w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
   w.best = w.g + kMaxDim;
+  w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(p + kWarpRegion) : nullptr;
   return w;
 }
 
 // --------------------------------------------------------------- K3 score
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT>
 __global__ void score_kernel(LigandView L, const double* __restrict__ genos, int n, int partition, int half_mode,
                              float* __restrict__ energy, float* __restrict__ grad, float* __restrict__ torque) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -46,12 +51,12 @@ __global__ void score_kernel(LigandView L, const double* __restrict__ genos, int
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * (blockDim.x >> 5) + warp;
   if (item >= n) return;
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const int dim = 6 + L.n_rot;
   const double* g = genos + (size_t)item * dim;
   Frame f;
-  const ScoreOut o = score_sums<METHOD, PAIR>(S, g, partition, half_mode != 0, w.ws, f);
-  for (int d = lane; d < dim; d += 32) grad[(size_t)item * dim + d] = project_dim(S, f, o, d);
+  const ScoreOut o = score_sums<METHOD, PAIR, EXACT>(S, g, partition, half_mode != 0, w.ws, f);
+  for (int d = lane; d < dim; d += 32) grad[(size_t)item * dim + d] = project_dim<EXACT>(S, f, o, d, w.ws);
   if (lane == 0) {
     energy[item] = o.sums[0];
     torque[3 * (size_t)item] = o.sums[4];
@@ -146,7 +151,7 @@ struct LsResult {
 
 // local_search docking.cpp:310-351 run by the calling warp.  start: global
 // or shared genotype.  On return w.best holds the best genotype.
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT>
 __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, int max_iters, double tol,
                                       int partition, bool half_mode, const WarpCtx& w) {
   const int lane = threadIdx.x & 31;
@@ -160,9 +165,9 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
   __syncwarp();
   double sg0 = 0.0, su0 = 0.0, sg1 = 0.0, su1 = 0.0;
   Frame f;
-  ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, partition, half_mode, w.ws, f);
-  float gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
-  float gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+  ScoreOut o = score_sums<METHOD, PAIR, EXACT>(S, w.g, partition, half_mode, w.ws, f);
+  float gr0 = lane < dim ? project_dim<EXACT>(S, f, o, lane, w.ws) : 0.f;
+  float gr1 = lane + 32 < dim ? project_dim<EXACT>(S, f, o, lane + 32, w.ws) : 0.f;
   LsResult r;
   r.energy = (double)o.sums[0];
   r.iterations = 0;
@@ -187,9 +192,9 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
       w.g[lane + 32] = x;
     }
     __syncwarp();
-    o = score_sums<METHOD, PAIR>(S, w.g, partition, half_mode, w.ws, f);
-    gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
-    gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+    o = score_sums<METHOD, PAIR, EXACT>(S, w.g, partition, half_mode, w.ws, f);
+    gr0 = lane < dim ? project_dim<EXACT>(S, f, o, lane, w.ws) : 0.f;
+    gr1 = lane + 32 < dim ? project_dim<EXACT>(S, f, o, lane + 32, w.ws) : 0.f;
     if ((double)o.sums[0] < r.energy) {
       r.energy = (double)o.sums[0];
       for (int d = lane; d < dim; d += 32) w.best[d] = w.g[d];
@@ -207,7 +212,7 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
   return r;
 }
 
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT>
 __global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n, int max_iters, double tol,
                           int partition, int half_mode, double* __restrict__ out_g, double* __restrict__ out_e,
                           int* __restrict__ out_it, int* __restrict__ out_cv, int* __restrict__ status) {
@@ -217,9 +222,9 @@ __global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * (blockDim.x >> 5) + warp;
   if (item >= n) return;
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const int dim = 6 + L.n_rot;
-  const LsResult r = local_search_warp<METHOD, PAIR>(S, starts + (size_t)item * dim, max_iters, tol, partition,
+  const LsResult r = local_search_warp<METHOD, PAIR, EXACT>(S, starts + (size_t)item * dim, max_iters, tol, partition,
                                                      half_mode != 0, w);
   for (int d = lane; d < dim; d += 32) out_g[(size_t)item * dim + d] = w.best[d];
   if (lane == 0) {
@@ -252,6 +257,7 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
   CtaCtx c;
   c.ws.tile = reinterpret_cast<__half*>(base);
   c.ws.rec = reinterpret_cast<float*>(base + 2 * 256 * 2);
+  c.ws.tq = nullptr;  // exact-torsion mode runs warp per pose only
   c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
   c.best = c.g + kMaxDim;
   c.part = c.best + kMaxDim;
@@ -331,8 +337,8 @@ __device__ LsResult local_search_cta(const SmemLigand& S, const double* start, i
         p.t = cross(d3{q[0], q[1], q[2]} - tr, p.g);
         return p;
       });
-      const float gr0 = lane < dim ? project_dim(S, f, o, lane) : 0.f;
-      const float gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32) : 0.f;
+      const float gr0 = lane < dim ? project_dim(S, f, o, lane, c.ws) : 0.f;
+      const float gr1 = lane + 32 < dim ? project_dim(S, f, o, lane + 32, c.ws) : 0.f;
       const double e = (double)o.sums[0];
       bool done = false;
       if (iter == 0) {
@@ -416,7 +422,7 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
   const int item = blockIdx.x * (blockDim.x >> 5) + warp;
   if (item >= D.R * D.P) return;
   const int run = item / D.P, p = item % D.P;
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const uint64_t key = run_key(D, run);
   for (int d = lane; d < D.dim; d += 32) {
     const uint64_t n = (uint64_t)p * D.dim + d + 1;
@@ -449,7 +455,7 @@ __global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
   if (item >= D.R * D.off) return;
   const int run = item / D.off, i = item % D.off;
   if (!D.active[run]) return;
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const int c = D.cur[run];
   const double* pop = D.pop[c] + (size_t)run * D.P * D.dim;
   const double* pe = D.pope[c] + (size_t)run * D.P;
@@ -519,7 +525,7 @@ __global__ void lga_ls_cta_kernel(LigandView L, LgaDev D) {
 
 // Lamarckian step: the r-th best offspring (stable by index) refined by a
 // device-resident local search (docking.cpp:476-489).
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT>
 __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
@@ -529,11 +535,11 @@ __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
   if (item >= D.R * D.L) return;
   const int run = item / D.L, r = item % D.L;
   if (!D.active[run]) return;
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const int c = D.cur[run];
   const int target = ls_target(D, run, r);
   const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
-  const LsResult res = local_search_warp<METHOD, PAIR>(S, start, D.ls_iters, D.tol, D.partition,
+  const LsResult res = local_search_warp<METHOD, PAIR, EXACT>(S, start, D.ls_iters, D.tol, D.partition,
                                                        D.half_mode != 0, w);
   const size_t o = (size_t)run * D.L + r;
   for (int d = lane; d < D.dim; d += 32) D.lsg[o * D.dim + d] = w.best[d];
@@ -645,7 +651,7 @@ __global__ void lga_gen_finalize(LgaDev D, int gen) {
 }
 
 // Final polish from the incumbent best (docking.cpp:501-515), warp per run.
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT>
 __global__ void lga_polish_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
@@ -659,8 +665,8 @@ __global__ void lga_polish_kernel(LigandView L, LgaDev D) {
     return;
   }
   const int iters = (int)((long long)D.ls_iters < remaining - 1 ? (long long)D.ls_iters : remaining - 1);
-  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp);
-  const LsResult res = local_search_warp<METHOD, PAIR>(S, D.best_g + (size_t)run * D.dim, iters, D.tol,
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
+  const LsResult res = local_search_warp<METHOD, PAIR, EXACT>(S, D.best_g + (size_t)run * D.dim, iters, D.tol,
                                                        D.partition, D.half_mode != 0, w);
   if (lane == 0) {
     if (res.status != MDR_OK) {
@@ -719,7 +725,7 @@ __global__ void lga_total_evals(LgaDev D, long long* out) {
 }
 
 // ------------------------------------------------------------ host side
-static size_t warp_smem(const LigandView& L, int wpb) { return ligand_smem_bytes(L) + (size_t)wpb * kWarpRegion; }
+static size_t warp_smem(const LigandView& L, int wpb) { return ligand_smem_bytes(L) + (size_t)wpb * warp_region_bytes(L); }
 
 template <class K>
 static cudaError_t prep(K kernel, size_t smem) {
@@ -757,14 +763,64 @@ static cudaError_t prep(K kernel, size_t smem) {
     }                                                                                                \
   }
 
-MDR_GEN_DISPATCH(score_kernel)
-MDR_GEN_DISPATCH(ls_kernel)
+// Kernels with an exact-torsion variant: the flag (LigandView::exact_torsion)
+// selects a separate instantiation, so the default kernels carry no trace of it.
+#define MDR_GEN_DISPATCH_EXACT(KERNEL)                                                                   \
+  template <bool X>                                                                                      \
+  struct KERNEL##_x {                                                                                    \
+    template <int M, int P>                                                                              \
+    static constexpr auto k = KERNEL<M, P, X>;                                                           \
+  };                                                                                                     \
+  template <class... A>                                                                                  \
+  static void dispatch_##KERNEL(int method, int pair, bool exact, dim3 g, dim3 b, size_t smem,           \
+                                cudaStream_t s, A... args) {                                             \
+    if (exact)                                                                                           \
+      dispatch_mp<KERNEL##_x<true>>(method, pair, g, b, smem, s, args...);                               \
+    else                                                                                                 \
+      dispatch_mp<KERNEL##_x<false>>(method, pair, g, b, smem, s, args...);                              \
+  }                                                                                                      \
+  static cudaError_t prep_##KERNEL(int method, int pair, bool exact, size_t smem) {                      \
+    return exact ? prep_mp<KERNEL##_x<true>>(method, pair, smem) : prep_mp<KERNEL##_x<false>>(method, pair, smem); \
+  }
+
+template <class T, class... A>
+static void dispatch_mp(int method, int pair, dim3 g, dim3 b, size_t smem, cudaStream_t s, A... args) {
+  switch (method * 3 + pair) {
+    case 0: T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;
+    case 1: T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;
+    case 2: T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;
+    case 3: T::template k<MDR_METHOD_TCU, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;
+    case 4: T::template k<MDR_METHOD_TCU, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;
+    case 5: T::template k<MDR_METHOD_TCU, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;
+    case 6: T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64><<<g, b, smem, s>>>(args...); break;
+    case 7: T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32><<<g, b, smem, s>>>(args...); break;
+    default: T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64_FAST><<<g, b, smem, s>>>(args...); break;
+  }
+}
+
+template <class T>
+static cudaError_t prep_mp(int method, int pair, size_t smem) {
+  switch (method * 3 + pair) {
+    case 0: return prep(T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP64>, smem);
+    case 1: return prep(T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP32>, smem);
+    case 2: return prep(T::template k<MDR_METHOD_BASELINE, MDR_PAIR_FP64_FAST>, smem);
+    case 3: return prep(T::template k<MDR_METHOD_TCU, MDR_PAIR_FP64>, smem);
+    case 4: return prep(T::template k<MDR_METHOD_TCU, MDR_PAIR_FP32>, smem);
+    case 5: return prep(T::template k<MDR_METHOD_TCU, MDR_PAIR_FP64_FAST>, smem);
+    case 6: return prep(T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64>, smem);
+    case 7: return prep(T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP32>, smem);
+    default: return prep(T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64_FAST>, smem);
+  }
+}
+
+MDR_GEN_DISPATCH_EXACT(score_kernel)
+MDR_GEN_DISPATCH_EXACT(ls_kernel)
 MDR_GEN_DISPATCH(ls_cta_kernel)
 MDR_GEN_DISPATCH(lga_init_kernel)
 MDR_GEN_DISPATCH(lga_offspring_kernel)
-MDR_GEN_DISPATCH(lga_ls_kernel)
+MDR_GEN_DISPATCH_EXACT(lga_ls_kernel)
 MDR_GEN_DISPATCH(lga_ls_cta_kernel)
-MDR_GEN_DISPATCH(lga_polish_kernel)
+MDR_GEN_DISPATCH_EXACT(lga_polish_kernel)
 MDR_GEN_DISPATCH(lga_polish_cta_kernel)
 
 static inline int blocks_for(long long items, int wpb) { return (int)((items + wpb - 1) / wpb); }
@@ -774,9 +830,9 @@ cudaError_t launch_score(const LigandView& L, const double* genos, int n, int me
                          int half_mode, float* energy, float* grad, float* torque, cudaStream_t s, int wpb) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = warp_smem(L, wpb);
-  cudaError_t e = prep_score_kernel(method, pair, smem);
+  cudaError_t e = prep_score_kernel(method, pair, L.exact_torsion != 0, smem);
   if (e != cudaSuccess) return e;
-  dispatch_score_kernel(method, pair, blocks_for(n, wpb), 32 * wpb, smem, s, L, genos, n, partition, half_mode,
+  dispatch_score_kernel(method, pair, L.exact_torsion != 0, blocks_for(n, wpb), 32 * wpb, smem, s, L, genos, n, partition, half_mode,
                         energy, grad, torque);
   return cudaGetLastError();
 }
@@ -811,9 +867,9 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
                            half_mode, out_g, out_e, out_it, out_cv, status);
   } else {
     const size_t smem = warp_smem(L, wpb);
-    e = prep_ls_kernel(method, pair, smem);
+    e = prep_ls_kernel(method, pair, L.exact_torsion != 0, smem);
     if (e != cudaSuccess) return e;
-    dispatch_ls_kernel(method, pair, blocks_for(n, wpb), 32 * wpb, smem, s, L, starts, n, max_iters, tol, partition,
+    dispatch_ls_kernel(method, pair, L.exact_torsion != 0, blocks_for(n, wpb), 32 * wpb, smem, s, L, starts, n, max_iters, tol, partition,
                        half_mode, out_g, out_e, out_it, out_cv, status);
   }
   return cudaGetLastError();
@@ -824,24 +880,25 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
 #ifndef MDR_POLISH_CTA
 #define MDR_POLISH_CTA 4  // measured: 0 / 2 / 4 / 8 -> 139.3 / 139.4 / 141.3 / 141.3 M evals/s on C3
 #endif
-static int polish_warps(int pair, int cta_warps) {
+static int polish_warps(const LigandView& L, int pair, int cta_warps) {
+  if (L.exact_torsion) return 0;  // exact-torsion staging lives in the warp-per-pose region
   return cta_warps > 0 ? cta_warps : (pair != MDR_PAIR_FP64 ? MDR_POLISH_CTA : 0);
 }
 
 cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps) {
   const size_t smem = warp_smem(L, wpb);
-  const int pw = polish_warps(pair, cta_warps);
+  const int pw = polish_warps(L, pair, cta_warps);
   cudaError_t e = prep_lga_init_kernel(method, pair, smem);
   if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, smem);
   if (cta_warps > 0) {
     if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
   } else {
-    if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, smem);
+    if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, L.exact_torsion != 0, smem);
   }
   if (pw > 0) {
     if (e == cudaSuccess) e = prep_lga_polish_cta_kernel(method, pair, cta_smem(L, pw));
   } else {
-    if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, smem);
+    if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, L.exact_torsion != 0, smem);
   }
   return e;
 }
@@ -868,18 +925,18 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
       else
-        dispatch_lga_ls_kernel(method, pair, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
+        dispatch_lga_ls_kernel(method, pair, L.exact_torsion != 0, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
     }
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
     lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
     launches += D.L > 0 ? 3 : 2;
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
-  const int pw = polish_warps(pair, cta_warps);
+  const int pw = polish_warps(L, pair, cta_warps);
   if (pw > 0)
     dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * pw, cta_smem(L, pw), s, L, D);
   else
-    dispatch_lga_polish_kernel(method, pair, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
+    dispatch_lga_polish_kernel(method, pair, L.exact_torsion != 0, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;

@@ -30,6 +30,7 @@ struct Ctx {
 
 thread_local int t_device = 0;
 thread_local int t_pair = MDR_PAIR_FP64_FAST;
+thread_local int t_exact = 0;
 
 mdr_ctx* ctx() {
   thread_local std::unique_ptr<Ctx> holder;
@@ -40,6 +41,7 @@ mdr_ctx* ctx() {
     if (!holder->c) throw DeviceError("mdr_ctx_create failed: no usable CUDA device " + std::to_string(t_device));
   }
   mdr_ctx_set_pair_precision(holder->c, t_pair);
+  mdr_ctx_set_exact_torsion(holder->c, t_exact);
   return holder->c;
 }
 
@@ -585,6 +587,8 @@ void set_device(int device) { t_device = device; }
 void set_pair_mode(PairMode m) {
   t_pair = m == PairMode::Reference ? MDR_PAIR_FP64 : m == PairMode::Fp32 ? MDR_PAIR_FP32 : MDR_PAIR_FP64_FAST;
 }
+
+void set_exact_torsion(bool on) { t_exact = on ? 1 : 0; }
 
 std::vector<ScoreResult> score_batch(const LigandInstance& in, const std::vector<Genotype>& poses, ReduceMethod method,
                                      AccumMode accum, int partition) {

@@ -16,6 +16,7 @@ constexpr int kMaxRot = kMaxDim - 6;
 constexpr int kMaxSites = 2048;    // per-CTA shared-memory copy
 constexpr int kMaxAtoms = 4096;
 constexpr int kWindow = 16;        // local_search convergence window, docking.cpp:314
+constexpr int kMaxExactAtoms = 1024;  // exact-torsion mode stages one float4 torque per atom per warp
 
 // One receptor site with the two pair-loop constants precomputed on the host
 // in the reference's evaluation order (docking.cpp:114-116):
@@ -26,7 +27,8 @@ struct SiteD {
 
 // Device view of an uploaded ligand / receptor pair.
 struct LigandView {
-  int n_atoms, n_sites, n_rot, pad;
+  int n_atoms, n_sites, n_rot;
+  int exact_torsion;  // 1: torsion gradient = exact per-group torque (mdr_ctx_set_exact_torsion)
   const SiteD* sites;
   const double4* atoms;  // local x, y, z, weight
   const int* tors;

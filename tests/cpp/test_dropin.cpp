@@ -349,6 +349,17 @@ static void extensions() {
   CHECK(scr.size() == 2 && scr[0].best_energy == scr[1].best_energy);
   for (int k = 0; k < 4; ++k) CHECK(scr[0].best_energy[static_cast<std::size_t>(k)] == runs[static_cast<std::size_t>(k)].best_energy);
   CHECK(scr[0].clusters.cluster_of == c.cluster_of && scr[0].clusters.n_clusters == c.n_clusters);
+  // exact-torsion mode: torsion entries follow score_reference's per-group torque
+  b200::set_exact_torsion(true);
+  const auto ex = b200::score_batch(s3, {g}, ReduceMethod::Baseline, AccumMode::Single, 64);
+  b200::set_exact_torsion(false);
+  const auto ap = b200::score_batch(s3, {g}, ReduceMethod::Baseline, AccumMode::Single, 64);
+  const RefScore rs = score_reference(s3, g);
+  double scale = 1.0, err = 0.0;
+  for (double v : rs.gradient) scale = std::max(scale, std::abs(v));
+  for (std::size_t d = 6; d < rs.gradient.size(); ++d) err = std::max(err, std::abs(ex[0].gradient[d] - rs.gradient[d]));
+  CHECK(err <= 2e-6 * scale);
+  CHECK(ex[0].energy == ap[0].energy && ex[0].gradient[3] == ap[0].gradient[3]);
 }
 
 int main(int argc, char** argv) {
