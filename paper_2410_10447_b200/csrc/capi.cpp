@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "dock_launch.h"
 #include "mdr.h"
 #include "mdr_shared.h"
@@ -50,6 +52,8 @@ struct mdr_ctx {
   int wpb = 2;        // warps per CTA of the warp-per-pose kernels
   int cta_warps = 0;  // 0: warp per pose (fastest measured); >0: CTA-per-pose LS
   int exact = 0;      // analytic mode: exact per-group torsion gradient (mdr_ctx_set_exact_torsion)
+  int chunking = 1;   // FP64-fast: chunked site mapping for small ligands (MDR_CHUNKING=0 disables)
+  int chunk_len = 0;  // > 0: pin the chunk length (MDR_CHUNK_LEN, timing only)
 
   std::string err;
   uint64_t launches = 0;
@@ -187,9 +191,42 @@ int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 || c->exac
 
 // The analytic-mode ligand view a launch uses: the instance's arrays plus the
 // context's torsion-gradient mode.
+// Site chunking of the FP64-fast warp-per-pose evaluation (mdr_device.cuh
+// score_sums): lane per atom leaves 32 - n_atoms lanes idle in the site loop
+// of a small ligand, so the sites are split into chunks of `len` (a multiple
+// of the kernel's ILP batch MDR_PV_CHUNK, so no chunk runs a scalar tail
+// unless n_sites itself is ragged) and the n_atoms x n_chunks (atom, chunk)
+// items spread over the 32 lanes.  len minimises the per-lane cost
+// rounds x (len + 4 sites' worth of staging and shorter ILP), with at most
+// kMaxChunkItems items; 1 chunk keeps lane per atom.  C3 (20 atoms x 64
+// sites) measured: lane per atom 145.8, len 8 / 16 / 24 / 32 -> 148.0 /
+// 146.3 / 150.4 / 130.0 M evals/s; the model picks 24.  `force_len` > 0
+// pins len (timing).
+void pick_chunks(int na, int ns, int force_len, int& n_chunks, int& chunk_len) {
+  constexpr int kBatch = 8;  // MDR_PV_CHUNK
+  n_chunks = 1;
+  chunk_len = ns;
+  long best = (long)((na + 31) / 32) * ns;
+  for (int len = kBatch; len < ns; len += kBatch) {
+    const int n = (ns + len - 1) / len;
+    if (na * n > kMaxChunkItems) continue;
+    const long cost = (long)((na * n + 31) / 32) * (len + 4);
+    if (force_len > 0 ? len == force_len : cost < best) {
+      best = cost;
+      n_chunks = n;
+      chunk_len = len;
+      if (force_len > 0) break;
+    }
+  }
+}
+
 LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   LigandView L = di->view;
   L.exact_torsion = c->exact;
+  L.n_chunks = 1;
+  L.chunk_len = L.n_sites;
+  if (c->pair == MDR_PAIR_FP64_FAST && c->chunking)
+    pick_chunks(L.n_atoms, L.n_sites, c->chunk_len, L.n_chunks, L.chunk_len);
   return L;
 }
 
@@ -215,6 +252,8 @@ mdr_ctx* mdr_ctx_create(int device) {
     return nullptr;
   }
   c->stream = c->own;
+  if (const char* v = std::getenv("MDR_CHUNKING")) c->chunking = std::atoi(v) != 0;  // A/B timing knobs
+  if (const char* v = std::getenv("MDR_CHUNK_LEN")) c->chunk_len = std::atoi(v);
   return c;
 }
 

@@ -18,6 +18,20 @@
 namespace mdr {
 
 // Per-warp shared-memory region: scratch | genotype | best genotype.
+// Register-allocation hint for the warp-per-pose search kernels (at most 16
+// warps per CTA).  Without it ptxas gives the chunked-site variant 100
+// registers and a 2-site-deep schedule (117 M evals/s on C3); with it, 128
+// registers and the latency hidden (150 M).  The lane-per-atom variant is
+// unaffected (126 -> 128 registers, same speed).
+#ifndef MDR_LS_LB
+#define MDR_LS_LB 1
+#endif
+#if MDR_LS_LB > 0
+#define MDR_LS_BOUNDS __launch_bounds__(512, MDR_LS_LB)
+#else
+#define MDR_LS_BOUNDS
+#endif
+
 constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8;
 
 struct WarpCtx {
@@ -27,7 +41,8 @@ struct WarpCtx {
 };
 
 __host__ __device__ inline size_t warp_region_bytes(const LigandView& L) {
-  return (size_t)kWarpRegion + (L.exact_torsion ? (size_t)16 * L.n_atoms : 0);
+  return (size_t)kWarpRegion + (L.exact_torsion ? (size_t)16 * L.n_atoms : 0) +
+         (L.n_chunks > 1 ? (size_t)32 * L.n_atoms * (1 + L.n_chunks) : 0);
 }
 
 __device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, const LigandView& L) {
@@ -37,13 +52,17 @@ __device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, co
   w.ws.rec = reinterpret_cast<float*>(p + 2 * 256 * 2);
   w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
   w.best = w.g + kMaxDim;
-  w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(p + kWarpRegion) : nullptr;
+  unsigned char* q = p + kWarpRegion;
+  w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(q) : nullptr;
+  if (L.exact_torsion) q += (size_t)16 * L.n_atoms;
+  w.ws.wpos = L.n_chunks > 1 ? reinterpret_cast<double4*>(q) : nullptr;
+  w.ws.part = L.n_chunks > 1 ? reinterpret_cast<double4*>(q) + L.n_atoms : nullptr;
   return w;
 }
 
 // --------------------------------------------------------------- K3 score
-template <int METHOD, int PAIR, bool EXACT>
-__global__ void score_kernel(LigandView L, const double* __restrict__ genos, int n, int partition, int half_mode,
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void MDR_LS_BOUNDS score_kernel(LigandView L, const double* __restrict__ genos, int n, int partition, int half_mode,
                              float* __restrict__ energy, float* __restrict__ grad, float* __restrict__ torque) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
@@ -55,7 +74,7 @@ __global__ void score_kernel(LigandView L, const double* __restrict__ genos, int
   const int dim = 6 + L.n_rot;
   const double* g = genos + (size_t)item * dim;
   Frame f;
-  const ScoreOut o = score_sums<METHOD, PAIR, EXACT>(S, g, partition, half_mode != 0, w.ws, f);
+  const ScoreOut o = score_sums<METHOD, PAIR, EXACT, CHUNK>(S, g, partition, half_mode != 0, w.ws, f);
   for (int d = lane; d < dim; d += 32) grad[(size_t)item * dim + d] = project_dim<EXACT>(S, f, o, d, w.ws);
   if (lane == 0) {
     energy[item] = o.sums[0];
@@ -151,7 +170,7 @@ struct LsResult {
 
 // local_search docking.cpp:310-351 run by the calling warp.  start: global
 // or shared genotype.  On return w.best holds the best genotype.
-template <int METHOD, int PAIR, bool EXACT>
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
 __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, int max_iters, double tol,
                                       int partition, bool half_mode, const WarpCtx& w) {
   const int lane = threadIdx.x & 31;
@@ -165,7 +184,7 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
   __syncwarp();
   double sg0 = 0.0, su0 = 0.0, sg1 = 0.0, su1 = 0.0;
   Frame f;
-  ScoreOut o = score_sums<METHOD, PAIR, EXACT>(S, w.g, partition, half_mode, w.ws, f);
+  ScoreOut o = score_sums<METHOD, PAIR, EXACT, CHUNK>(S, w.g, partition, half_mode, w.ws, f);
   float gr0 = lane < dim ? project_dim<EXACT>(S, f, o, lane, w.ws) : 0.f;
   float gr1 = lane + 32 < dim ? project_dim<EXACT>(S, f, o, lane + 32, w.ws) : 0.f;
   LsResult r;
@@ -192,7 +211,7 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
       w.g[lane + 32] = x;
     }
     __syncwarp();
-    o = score_sums<METHOD, PAIR, EXACT>(S, w.g, partition, half_mode, w.ws, f);
+    o = score_sums<METHOD, PAIR, EXACT, CHUNK>(S, w.g, partition, half_mode, w.ws, f);
     gr0 = lane < dim ? project_dim<EXACT>(S, f, o, lane, w.ws) : 0.f;
     gr1 = lane + 32 < dim ? project_dim<EXACT>(S, f, o, lane + 32, w.ws) : 0.f;
     if ((double)o.sums[0] < r.energy) {
@@ -212,8 +231,8 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
   return r;
 }
 
-template <int METHOD, int PAIR, bool EXACT>
-__global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n, int max_iters, double tol,
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void MDR_LS_BOUNDS ls_kernel(LigandView L, const double* __restrict__ starts, int n, int max_iters, double tol,
                           int partition, int half_mode, double* __restrict__ out_g, double* __restrict__ out_e,
                           int* __restrict__ out_it, int* __restrict__ out_cv, int* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -224,7 +243,7 @@ __global__ void ls_kernel(LigandView L, const double* __restrict__ starts, int n
   if (item >= n) return;
   WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
   const int dim = 6 + L.n_rot;
-  const LsResult r = local_search_warp<METHOD, PAIR, EXACT>(S, starts + (size_t)item * dim, max_iters, tol, partition,
+  const LsResult r = local_search_warp<METHOD, PAIR, EXACT, CHUNK>(S, starts + (size_t)item * dim, max_iters, tol, partition,
                                                      half_mode != 0, w);
   for (int d = lane; d < dim; d += 32) out_g[(size_t)item * dim + d] = w.best[d];
   if (lane == 0) {
@@ -258,6 +277,7 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
   c.ws.tile = reinterpret_cast<__half*>(base);
   c.ws.rec = reinterpret_cast<float*>(base + 2 * 256 * 2);
   c.ws.tq = nullptr;  // exact-torsion mode runs warp per pose only
+  c.ws.wpos = c.ws.part = nullptr;
   c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
   c.best = c.g + kMaxDim;
   c.part = c.best + kMaxDim;
@@ -413,7 +433,7 @@ __global__ void ls_cta_kernel(LigandView L, const double* __restrict__ starts, i
 
 // ------------------------------------------------------------- K5 LGA
 // lga init: random_genotype docking.cpp:360-388 + score, warp per individual.
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
 __global__ void lga_init_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
@@ -436,7 +456,7 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
   }
   __syncwarp();
   Frame f;
-  const ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
+  const ScoreOut o = score_sums<METHOD, PAIR, false, CHUNK>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
   if (lane == 0) D.pope[0][(size_t)run * D.P + p] = (double)o.sums[0];
 }
 
@@ -445,7 +465,7 @@ __global__ void lga_init_kernel(LigandView L, LgaDev D) {
 // arithmetic crossover, Gaussian mutation, angle normalisation, score
 // (docking.cpp:437-472).  Draw offsets: every generation consumes
 // off * (4 + 3*dim) draws after the P*dim initial ones.
-template <int METHOD, int PAIR>
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
 __global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
@@ -490,7 +510,7 @@ __global__ void lga_offspring_kernel(LigandView L, LgaDev D, int gen) {
   }
   __syncwarp();
   Frame f;
-  const ScoreOut o = score_sums<METHOD, PAIR>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
+  const ScoreOut o = score_sums<METHOD, PAIR, false, CHUNK>(S, w.g, D.partition, D.half_mode != 0, w.ws, f);
   if (lane == 0) ne[1 + i] = (double)o.sums[0];
 }
 
@@ -525,8 +545,8 @@ __global__ void lga_ls_cta_kernel(LigandView L, LgaDev D) {
 
 // Lamarckian step: the r-th best offspring (stable by index) refined by a
 // device-resident local search (docking.cpp:476-489).
-template <int METHOD, int PAIR, bool EXACT>
-__global__ void lga_ls_kernel(LigandView L, LgaDev D) {
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void MDR_LS_BOUNDS lga_ls_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
   __syncthreads();
@@ -539,7 +559,7 @@ __global__ void lga_ls_kernel(LigandView L, LgaDev D) {
   const int c = D.cur[run];
   const int target = ls_target(D, run, r);
   const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
-  const LsResult res = local_search_warp<METHOD, PAIR, EXACT>(S, start, D.ls_iters, D.tol, D.partition,
+  const LsResult res = local_search_warp<METHOD, PAIR, EXACT, CHUNK>(S, start, D.ls_iters, D.tol, D.partition,
                                                        D.half_mode != 0, w);
   const size_t o = (size_t)run * D.L + r;
   for (int d = lane; d < D.dim; d += 32) D.lsg[o * D.dim + d] = w.best[d];
@@ -651,8 +671,8 @@ __global__ void lga_gen_finalize(LgaDev D, int gen) {
 }
 
 // Final polish from the incumbent best (docking.cpp:501-515), warp per run.
-template <int METHOD, int PAIR, bool EXACT>
-__global__ void lga_polish_kernel(LigandView L, LgaDev D) {
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void MDR_LS_BOUNDS lga_polish_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
   __syncthreads();
@@ -666,7 +686,7 @@ __global__ void lga_polish_kernel(LigandView L, LgaDev D) {
   }
   const int iters = (int)((long long)D.ls_iters < remaining - 1 ? (long long)D.ls_iters : remaining - 1);
   WarpCtx w = warp_region(smem + ligand_smem_bytes(L), warp, L);
-  const LsResult res = local_search_warp<METHOD, PAIR, EXACT>(S, D.best_g + (size_t)run * D.dim, iters, D.tol,
+  const LsResult res = local_search_warp<METHOD, PAIR, EXACT, CHUNK>(S, D.best_g + (size_t)run * D.dim, iters, D.tol,
                                                        D.partition, D.half_mode != 0, w);
   if (lane == 0) {
     if (res.status != MDR_OK) {
@@ -766,21 +786,50 @@ static cudaError_t prep(K kernel, size_t smem) {
 // Kernels with an exact-torsion variant: the flag (LigandView::exact_torsion)
 // selects a separate instantiation, so the default kernels carry no trace of it.
 #define MDR_GEN_DISPATCH_EXACT(KERNEL)                                                                   \
-  template <bool X>                                                                                      \
+  template <bool X, bool CH>                                                                             \
   struct KERNEL##_x {                                                                                    \
     template <int M, int P>                                                                              \
-    static constexpr auto k = KERNEL<M, P, X>;                                                           \
+    static constexpr auto k = KERNEL<M, P, X, CH && P == MDR_PAIR_FP64_FAST>;                            \
   };                                                                                                     \
   template <class... A>                                                                                  \
-  static void dispatch_##KERNEL(int method, int pair, bool exact, dim3 g, dim3 b, size_t smem,           \
+  static void dispatch_##KERNEL(int method, int pair, const LigandView& L, dim3 g, dim3 b, size_t smem,  \
                                 cudaStream_t s, A... args) {                                             \
-    if (exact)                                                                                           \
+    const bool x = L.exact_torsion != 0, ch = L.n_chunks > 1;                           \
+    if (x && ch)                                                                                         \
+      dispatch_mp<KERNEL##_x<true, true>>(method, pair, g, b, smem, s, args...);                         \
+    else if (x)                                                                                          \
+      dispatch_mp<KERNEL##_x<true, false>>(method, pair, g, b, smem, s, args...);                        \
+    else if (ch)                                                                                         \
+      dispatch_mp<KERNEL##_x<false, true>>(method, pair, g, b, smem, s, args...);                        \
+    else                                                                                                 \
+      dispatch_mp<KERNEL##_x<false, false>>(method, pair, g, b, smem, s, args...);                       \
+  }                                                                                                      \
+  static cudaError_t prep_##KERNEL(int method, int pair, const LigandView& L, size_t smem) {             \
+    const bool x = L.exact_torsion != 0, ch = L.n_chunks > 1;                           \
+    if (x && ch) return prep_mp<KERNEL##_x<true, true>>(method, pair, smem);                             \
+    if (x) return prep_mp<KERNEL##_x<true, false>>(method, pair, smem);                                  \
+    if (ch) return prep_mp<KERNEL##_x<false, true>>(method, pair, smem);                                 \
+    return prep_mp<KERNEL##_x<false, false>>(method, pair, smem);                                        \
+  }
+
+// Kernels that only score (no gradient projection): chunking variant only.
+#define MDR_GEN_DISPATCH_CHUNK(KERNEL)                                                                   \
+  template <bool CH>                                                                                     \
+  struct KERNEL##_x {                                                                                    \
+    template <int M, int P>                                                                              \
+    static constexpr auto k = KERNEL<M, P, false, CH && P == MDR_PAIR_FP64_FAST>;                        \
+  };                                                                                                     \
+  template <class... A>                                                                                  \
+  static void dispatch_##KERNEL(int method, int pair, const LigandView& L, dim3 g, dim3 b, size_t smem,  \
+                                cudaStream_t s, A... args) {                                             \
+    if (L.n_chunks > 1)                                                                 \
       dispatch_mp<KERNEL##_x<true>>(method, pair, g, b, smem, s, args...);                               \
     else                                                                                                 \
       dispatch_mp<KERNEL##_x<false>>(method, pair, g, b, smem, s, args...);                              \
   }                                                                                                      \
-  static cudaError_t prep_##KERNEL(int method, int pair, bool exact, size_t smem) {                      \
-    return exact ? prep_mp<KERNEL##_x<true>>(method, pair, smem) : prep_mp<KERNEL##_x<false>>(method, pair, smem); \
+  static cudaError_t prep_##KERNEL(int method, int pair, const LigandView& L, size_t smem) {             \
+    return L.n_chunks > 1 ? prep_mp<KERNEL##_x<true>>(method, pair, smem)                                \
+                          : prep_mp<KERNEL##_x<false>>(method, pair, smem);                              \
   }
 
 template <class T, class... A>
@@ -816,8 +865,8 @@ static cudaError_t prep_mp(int method, int pair, size_t smem) {
 MDR_GEN_DISPATCH_EXACT(score_kernel)
 MDR_GEN_DISPATCH_EXACT(ls_kernel)
 MDR_GEN_DISPATCH(ls_cta_kernel)
-MDR_GEN_DISPATCH(lga_init_kernel)
-MDR_GEN_DISPATCH(lga_offspring_kernel)
+MDR_GEN_DISPATCH_CHUNK(lga_init_kernel)
+MDR_GEN_DISPATCH_CHUNK(lga_offspring_kernel)
 MDR_GEN_DISPATCH_EXACT(lga_ls_kernel)
 MDR_GEN_DISPATCH(lga_ls_cta_kernel)
 MDR_GEN_DISPATCH_EXACT(lga_polish_kernel)
@@ -830,9 +879,9 @@ cudaError_t launch_score(const LigandView& L, const double* genos, int n, int me
                          int half_mode, float* energy, float* grad, float* torque, cudaStream_t s, int wpb) {
   if (n <= 0) return cudaSuccess;
   const size_t smem = warp_smem(L, wpb);
-  cudaError_t e = prep_score_kernel(method, pair, L.exact_torsion != 0, smem);
+  cudaError_t e = prep_score_kernel(method, pair, L, smem);
   if (e != cudaSuccess) return e;
-  dispatch_score_kernel(method, pair, L.exact_torsion != 0, blocks_for(n, wpb), 32 * wpb, smem, s, L, genos, n, partition, half_mode,
+  dispatch_score_kernel(method, pair, L, blocks_for(n, wpb), 32 * wpb, smem, s, L, genos, n, partition, half_mode,
                         energy, grad, torque);
   return cudaGetLastError();
 }
@@ -867,9 +916,9 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
                            half_mode, out_g, out_e, out_it, out_cv, status);
   } else {
     const size_t smem = warp_smem(L, wpb);
-    e = prep_ls_kernel(method, pair, L.exact_torsion != 0, smem);
+    e = prep_ls_kernel(method, pair, L, smem);
     if (e != cudaSuccess) return e;
-    dispatch_ls_kernel(method, pair, L.exact_torsion != 0, blocks_for(n, wpb), 32 * wpb, smem, s, L, starts, n, max_iters, tol, partition,
+    dispatch_ls_kernel(method, pair, L, blocks_for(n, wpb), 32 * wpb, smem, s, L, starts, n, max_iters, tol, partition,
                        half_mode, out_g, out_e, out_it, out_cv, status);
   }
   return cudaGetLastError();
@@ -888,17 +937,17 @@ static int polish_warps(const LigandView& L, int pair, int cta_warps) {
 cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps) {
   const size_t smem = warp_smem(L, wpb);
   const int pw = polish_warps(L, pair, cta_warps);
-  cudaError_t e = prep_lga_init_kernel(method, pair, smem);
-  if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, smem);
+  cudaError_t e = prep_lga_init_kernel(method, pair, L, smem);
+  if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, L, smem);
   if (cta_warps > 0) {
     if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
   } else {
-    if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, L.exact_torsion != 0, smem);
+    if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, L, smem);
   }
   if (pw > 0) {
     if (e == cudaSuccess) e = prep_lga_polish_cta_kernel(method, pair, cta_smem(L, pw));
   } else {
-    if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, L.exact_torsion != 0, smem);
+    if (e == cudaSuccess) e = prep_lga_polish_kernel(method, pair, L, smem);
   }
   return e;
 }
@@ -914,18 +963,18 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
   const size_t cs = cta_smem(L, cta_warps > 0 ? cta_warps : 1);
   int launches = 0;
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 2], s);
-  dispatch_lga_init_kernel(method, pair, blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s, L, D);
+  dispatch_lga_init_kernel(method, pair, L, blocks_for((long long)D.R * D.P, wpb), 32 * wpb, smem, s, L, D);
   lga_init_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D);
   launches += 2;
   for (int gen = 0; gen < D.gens; ++gen) {
-    dispatch_lga_offspring_kernel(method, pair, blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s, L, D,
+    dispatch_lga_offspring_kernel(method, pair, L, blocks_for((long long)D.R * D.off, wpb), 32 * wpb, smem, s, L, D,
                                   gen);
     if (ls_events) cudaEventRecord(ls_events[2 * gen], s);
     if (D.L > 0) {
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
       else
-        dispatch_lga_ls_kernel(method, pair, L.exact_torsion != 0, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
+        dispatch_lga_ls_kernel(method, pair, L, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
     }
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
     lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
@@ -936,7 +985,7 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
   if (pw > 0)
     dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * pw, cta_smem(L, pw), s, L, D);
   else
-    dispatch_lga_polish_kernel(method, pair, L.exact_torsion != 0, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
+    dispatch_lga_polish_kernel(method, pair, L, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;

@@ -16,7 +16,8 @@ constexpr int kMaxRot = kMaxDim - 6;
 constexpr int kMaxSites = 2048;    // per-CTA shared-memory copy
 constexpr int kMaxAtoms = 4096;
 constexpr int kWindow = 16;        // local_search convergence window, docking.cpp:314
-constexpr int kMaxExactAtoms = 1024;  // exact-torsion mode stages one float4 torque per atom per warp
+constexpr int kMaxExactAtoms = 1024;
+constexpr int kMaxChunkItems = 256;   // atoms x site chunks staged per warp (32 B each)  // exact-torsion mode stages one float4 torque per atom per warp
 
 // One receptor site with the two pair-loop constants precomputed on the host
 // in the reference's evaluation order (docking.cpp:114-116):
@@ -29,6 +30,8 @@ struct SiteD {
 struct LigandView {
   int n_atoms, n_sites, n_rot;
   int exact_torsion;  // 1: torsion gradient = exact per-group torque (mdr_ctx_set_exact_torsion)
+  int n_chunks;       // FP64-fast: sites split into n_chunks ranges of chunk_len (1 = lane per atom)
+  int chunk_len;
   const SiteD* sites;
   const double4* atoms;  // local x, y, z, weight
   const int* tors;

@@ -279,3 +279,34 @@ def test_fast_modes_cta_local_search_and_lga(pair, port, instances, dev):
     mc = np.mean([r["best_energy"] for r in cpu])
     assert abs(mg - mc) / abs(mc) < 0.002
     fast.close()
+
+
+def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch):
+    """FP64-fast small ligands run the chunked site mapping (atoms x site
+    chunks over all 32 lanes, capi.cpp pick_chunks); MDR_CHUNKING=0 keeps
+    lane per atom.  The two differ only in FP64 summation order (chunk
+    partial sums), so: float outputs bit-identical for >= 99 % of
+    evaluations and within 1e-6 relative for all; every local search within
+    1e-5 relative; both against the CPU reference as in the tests above."""
+    chunked = Device(0, pair=PAIR_FP64_FAST)
+    monkeypatch.setenv("MDR_CHUNKING", "0")
+    lane = Device(0, pair=PAIR_FP64_FAST)
+    same = total = 0
+    for inst, poses in random_cases(91, 12, natoms_max=60, nsites_max=80):
+        ec, gc, _, _ = chunked.score_batch(inst, poses)
+        el, gl, _, _ = lane.score_batch(inst, poses)
+        total += len(poses)
+        same += int(np.sum((bits(ec) == bits(el)) & np.all(bits(gc) == bits(gl), axis=1)))
+        assert np.all(np.abs(ec - el) <= 1e-6 * np.maximum(np.abs(el), 1.0))
+        scale = np.maximum(np.abs(gl).max(axis=1, keepdims=True), 1.0)
+        assert np.all(np.abs(gc - gl) <= 1e-6 * scale)
+    assert same >= 0.99 * total, (same, total)
+    inst = instances["synth20"]
+    rng = derive_rng(17, "chunk/ls")
+    starts = np.stack([random_pose(rng, inst.n_rot, 0.6) for _ in range(32)])
+    rc = chunked.local_search_batch(inst, starts, 150, 1e-4, BASELINE, SINGLE, 64)
+    rl = lane.local_search_batch(inst, starts, 150, 1e-4, BASELINE, SINGLE, 64)
+    for a, b in zip(rc, rl):
+        assert abs(a.energy - b.energy) <= 1e-5 * max(abs(b.energy), 1.0)
+    chunked.close()
+    lane.close()
