@@ -52,9 +52,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
               f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("MDR_NVCC_EXTRA", "").split()  # experiments only
     objs, procs = [], []
+    headers = [f for f in _deps() if f not in sources()]
+    flags_file = os.path.join(objdir, "flags.txt")
+    flags = " ".join(common)
+    same_flags = os.path.exists(flags_file) and open(flags_file).read() == flags
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
+        # incremental: an object newer than its source and every header, built
+        # with the same flags, is reused (a header change rebuilds everything)
+        if (not force and same_flags and os.path.exists(obj)
+                and all(os.path.getmtime(f) <= os.path.getmtime(obj) for f in [src] + headers)):
+            continue
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
         else:  # host-only C++ (C-ABI, drop-in C++ API): g++, C++20, no FP contraction
@@ -67,6 +76,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}:\n{out}")
         if verbose and out:
             print(out)
+    with open(flags_file, "w") as f:
+        f.write(flags)
     link = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-Xcompiler", "-pthread", "-o", LIB, *objs,
             "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     p = subprocess.run(link, capture_output=True, text=True)
