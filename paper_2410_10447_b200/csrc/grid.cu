@@ -288,6 +288,11 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
   // partner chunk u % C); the pair energy is shared by both ends when both
   // atoms are torsioned (each end visits it), whole when the partner is rigid.
   if (intra) {
+    // partners in flight per thread: the best measured per method on C4
+    // (Baseline 2/4/6/8 -> 53.9/55.1/54.5/54.9 M evals/s; Tcu 41.1/43.0/
+    // 51.5/51.1; TcuSplit 41.2/42.5/42.5/42.9 — ptxas schedules the loop
+    // differently next to each reduction)
+    constexpr int kUnroll = METHOD == MDR_METHOD_TCU ? 6 : METHOD == MDR_METHOD_TCU_SPLIT ? 8 : 4;
     const int C = S.C, U = S.nta * C;
     for (int u = tid; u < U; u += T) {
       const int a = S.grp_atoms[u / C];
@@ -297,7 +302,7 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
       // branch-free: a same-group partner (incl. j == a) contributes with
       // weight 0 instead of a divergent `continue`; its u is offset by 1 so
       // the masked terms stay finite even for zero radii
-#pragma unroll 4
+#pragma unroll kUnroll
       for (int j = u % C; j < S.na; j += C) {
         const float4 pj = S.pos[j], cj = S.chem[j];
         const int gj = __float_as_int(pj.w);
