@@ -215,6 +215,20 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------ GPU arm
+def profiled_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture of this configuration (profiles/, written on the box
+    by tools/ncu_traffic.py), or None when absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ls_kernel_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return {"bytes_per_launch": d["dram_bytes_per_launch"], "kernel": d["kernel"], "source": "profiles/" +
+                os.path.basename(path)}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def fp64_peak_tflops(torch):
     """Live FP64 FMA peak of this GPU (DFMA chains, no memory traffic)."""
     src = r"""
@@ -406,7 +420,7 @@ def run_gpu_arm(args):
                                    "figure)",
                     "flop_per_eval": flop_per_eval(inst, settings.partition),
                     "ls_evals_per_step": ls_evals.value, "ls_kernel_ms_per_launch": ls_ms.value / n_ls_launches,
-                    "traffic": None}
+                    "traffic": profiled_traffic()}
             ls_share = ls_ms.value / all_ms.value
 
     if rank == 0:
