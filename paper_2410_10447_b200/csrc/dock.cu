@@ -546,7 +546,7 @@ __global__ void lga_ls_cta_kernel(LigandView L, LgaDev D) {
 // Lamarckian step: the r-th best offspring (stable by index) refined by a
 // device-resident local search (docking.cpp:476-489).
 template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
-__global__ void MDR_LS_BOUNDS lga_ls_kernel(LigandView L, LgaDev D) {
+__device__ __forceinline__ void lga_ls_body(const LigandView& L, const LgaDev& D) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SmemLigand S = load_ligand(L, smem);
   __syncthreads();
@@ -570,6 +570,18 @@ __global__ void MDR_LS_BOUNDS lga_ls_kernel(LigandView L, LgaDev D) {
     D.lstarget[o] = target;
     if (res.status != MDR_OK) D.status[run] = res.status;
   }
+}
+
+// The dominant kernel.  FP32 pair terms run without the register hint (the
+// hint costs that mode 218.7 -> 205.4 M evals/s; the FP64 modes and the
+// tensor-core reductions gain from it, TcuSplit 113 -> 150 M).
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void MDR_LS_BOUNDS lga_ls_kernel(LigandView L, LgaDev D) {
+  lga_ls_body<METHOD, PAIR, EXACT, CHUNK>(L, D);
+}
+template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+__global__ void lga_ls_kernel_nb(LigandView L, LgaDev D) {
+  lga_ls_body<METHOD, PAIR, EXACT, CHUNK>(L, D);
 }
 
 // First occurrence of the strict minimum of candidate energies e(0..n-1)
@@ -789,7 +801,7 @@ static cudaError_t prep(K kernel, size_t smem) {
   template <bool X, bool CH>                                                                             \
   struct KERNEL##_x {                                                                                    \
     template <int M, int P>                                                                              \
-    static constexpr auto k = KERNEL<M, P, X, CH && P == MDR_PAIR_FP64_FAST>;                            \
+    static constexpr auto k = KERNEL##_sel<M, P, X, CH && P == MDR_PAIR_FP64_FAST>::k();                 \
   };                                                                                                     \
   template <class... A>                                                                                  \
   static void dispatch_##KERNEL(int method, int pair, const LigandView& L, dim3 g, dim3 b, size_t smem,  \
@@ -861,6 +873,26 @@ static cudaError_t prep_mp(int method, int pair, size_t smem) {
     default: return prep(T::template k<MDR_METHOD_TCU_SPLIT, MDR_PAIR_FP64_FAST>, smem);
   }
 }
+
+// Kernel instantiation a dispatch uses: the kernel itself, except the
+// FP32-pair LGA search (lga_ls_kernel_nb, no register hint).
+#define MDR_SEL_DEFAULT(KERNEL)                              \
+  template <int M, int P, bool X, bool C>                    \
+  struct KERNEL##_sel {                                      \
+    static constexpr auto k() { return &KERNEL<M, P, X, C>; } \
+  };
+MDR_SEL_DEFAULT(score_kernel)
+MDR_SEL_DEFAULT(ls_kernel)
+MDR_SEL_DEFAULT(lga_polish_kernel)
+template <int M, int P, bool X, bool C>
+struct lga_ls_kernel_sel {
+  static constexpr auto k() {
+    if constexpr (P == MDR_PAIR_FP32)
+      return &lga_ls_kernel_nb<M, P, X, C>;
+    else
+      return &lga_ls_kernel<M, P, X, C>;
+  }
+};
 
 MDR_GEN_DISPATCH_EXACT(score_kernel)
 MDR_GEN_DISPATCH_EXACT(ls_kernel)
