@@ -292,7 +292,10 @@ def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch
     monkeypatch.setenv("MDR_CHUNKING", "0")
     lane = Device(0, pair=PAIR_FP64_FAST)
     same = total = 0
-    for inst, poses in random_cases(91, 12, natoms_max=60, nsites_max=80):
+    rng = derive_rng(92, "chunk/many-torsions")
+    wide = random_instance(rng, 40, 16, 64)  # 43 angles: the lane-trig table's second round
+    wide_poses = np.stack([random_pose(rng, wide.n_rot, 0.8) for _ in range(16)])
+    for inst, poses in random_cases(91, 12, natoms_max=60, nsites_max=80) + [(wide, wide_poses)]:
         ec, gc, _, _ = chunked.score_batch(inst, poses)
         el, gl, _, _ = lane.score_batch(inst, poses)
         total += len(poses)
