@@ -17,7 +17,6 @@
 
 namespace mdr {
 
-// Per-warp shared-memory region: scratch | genotype | best genotype.
 // Register-allocation hint for the warp-per-pose search kernels (at most 16
 // warps per CTA).  Without it ptxas gives the chunked-site variant 100
 // registers and a 2-site-deep schedule (117 M evals/s on C3); with it, 128
@@ -32,7 +31,9 @@ namespace mdr {
 #define MDR_LS_BOUNDS
 #endif
 
-constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8;
+// Per-warp shared-memory region: scratch | genotype | best genotype | angle
+// trig table | [exact-torsion torques] | [chunked: positions, chunk sums].
+constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16;
 
 struct WarpCtx {
   WarpScratch ws;
@@ -52,6 +53,7 @@ __device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, co
   w.ws.rec = reinterpret_cast<float*>(p + 2 * 256 * 2);
   w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
   w.best = w.g + kMaxDim;
+  w.ws.trig = reinterpret_cast<double2*>(w.best + kMaxDim);
   unsigned char* q = p + kWarpRegion;
   w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(q) : nullptr;
   if (L.exact_torsion) q += (size_t)16 * L.n_atoms;
@@ -278,6 +280,7 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
   c.ws.rec = reinterpret_cast<float*>(base + 2 * 256 * 2);
   c.ws.tq = nullptr;  // exact-torsion mode runs warp per pose only
   c.ws.wpos = c.ws.part = nullptr;
+  c.ws.trig = nullptr;
   c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
   c.best = c.g + kMaxDim;
   c.part = c.best + kMaxDim;
