@@ -32,6 +32,9 @@
 #ifndef MDR_GRID_F32_TRIG
 #define MDR_GRID_F32_TRIG 1
 #endif
+#ifndef MDR_GRID_UNROLL
+#define MDR_GRID_UNROLL 4  // partners in flight per thread in phase C
+#endif
 
 namespace mdr {
 
@@ -40,7 +43,8 @@ struct GridSmem {
   double4* atoms;   // na: local x, y, z, weight
   int* tors;        // na
   int* type;        // na
-  float4* chem;     // na
+  float4* chem;     // na: 1.25 radius, sqrt eps, q, energy share (1 rigid, 1/2 torsioned)
+  float* keq;       // na: k_e q (the unit side of the Coulomb term)
   double* taxes;    // 3 * nr
   int* grp_off;     // nr + 1
   int* grp_atoms;   // nta
@@ -70,6 +74,7 @@ __host__ __device__ inline size_t grid_smem_bytes(int na, int nr, int nta, int T
   b += al16(sizeof(double4) * na);
   b += al16(sizeof(int) * na) * 2;
   b += al16(sizeof(float4) * na);
+  b += al16(sizeof(float) * na);
   b += al16(sizeof(double) * 3 * (nr > 0 ? nr : 1));
   b += al16(sizeof(int) * (nr + 1));
   b += al16(sizeof(int) * (nta > 0 ? nta : 1));
@@ -100,6 +105,7 @@ __device__ GridSmem grid_load(const LigandView& L, const FlexView& F, unsigned c
   S.tors = reinterpret_cast<int*>(take(sizeof(int) * na));
   S.type = reinterpret_cast<int*>(take(sizeof(int) * na));
   S.chem = reinterpret_cast<float4*>(take(sizeof(float4) * na));
+  S.keq = reinterpret_cast<float*>(take(sizeof(float) * na));
   S.taxes = reinterpret_cast<double*>(take(sizeof(double) * 3 * (nr > 0 ? nr : 1)));
   S.grp_off = reinterpret_cast<int*>(take(sizeof(int) * (nr + 1)));
   S.grp_atoms = reinterpret_cast<int*>(take(sizeof(int) * (nta > 0 ? nta : 1)));
@@ -116,7 +122,11 @@ __device__ GridSmem grid_load(const LigandView& L, const FlexView& F, unsigned c
     S.atoms[i] = L.atoms[i];
     S.tors[i] = L.tors[i];
     S.type[i] = F.type[i];
-    S.chem[i] = F.chem[i];
+    // phase C's per-partner constants: radius pre-scaled by 1.25 (so
+    // d0'^2 = 1.5625 d0^2), the pair-energy share of this partner in w
+    const float4 ch = F.chem[i];
+    S.chem[i] = make_float4(1.25f * ch.x, ch.y, ch.z, L.tors[i] < 0 ? 1.0f : 0.5f);
+    S.keq[i] = ch.w;
   }
   for (int i = threadIdx.x; i < 3 * nr; i += blockDim.x) S.taxes[i] = L.taxes[i];
   for (int i = threadIdx.x; i <= nr; i += blockDim.x) S.grp_off[i] = F.grp_off[i];
@@ -288,16 +298,16 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
   // partner chunk u % C); the pair energy is shared by both ends when both
   // atoms are torsioned (each end visits it), whole when the partner is rigid.
   if (intra) {
-    // partners in flight per thread: the best measured per method on C4
-    // (Baseline 2/4/6/8 -> 53.9/55.1/54.5/54.9 M evals/s; Tcu 41.1/43.0/
-    // 51.5/51.1; TcuSplit 41.2/42.5/42.5/42.9 — ptxas schedules the loop
-    // differently next to each reduction)
-    constexpr int kUnroll = METHOD == MDR_METHOD_TCU ? 6 : METHOD == MDR_METHOD_TCU_SPLIT ? 8 : 4;
+    // partners in flight per thread (C4, unroll 2 / 4 / 6 / 8: Baseline
+    // 46.4 / 59.8 / 59.1 / 59.1 M evals/s, TcuSplit 54.4 / 54.9 / 54.8 /
+    // 55.0, Tcu 43.1 / 45.5 / 45.0 / 45.5)
+    constexpr int kUnroll = MDR_GRID_UNROLL;
     const int C = S.C, U = S.nta * C;
     for (int u = tid; u < U; u += T) {
       const int a = S.grp_atoms[u / C];
       const int ga = S.tors[a];
       const float4 pa = S.pos[a], ca = S.chem[a];
+      const float ea12 = -12.0f * ca.y, qa = S.keq[a];
       float fx = 0.f, fy = 0.f, fz = 0.f, ee = 0.f;
       // branch-free: a same-group partner (incl. j == a) contributes with
       // weight 0 instead of a divergent `continue`; its u is offset by 1 so
@@ -307,20 +317,20 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
         const float4 pj = S.pos[j], cj = S.chem[j];
         const int gj = __float_as_int(pj.w);
         const float dx = pa.x - pj.x, dy = pa.y - pj.y, dz = pa.z - pj.z;
-        const float d0 = ca.x + cj.x;
-        const float d02 = d0 * d0;
-        const float on = gj == ga ? 0.0f : 1.0f;
-        const float u2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, fmaf(0.5625f, d02, 1.0f - on))));
+        const float d0 = ca.x + cj.x;  // 1.25 (r_a + r_j)
+        const float d02 = d0 * d0;      // 1.5625 (r_a + r_j)^2
+        const bool same = gj == ga;
+        const float u2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, fmaf(0.36f, d02, same ? 1.0f : 0.0f))));
         float iu;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iu) : "f"(u2));
-        const float rho2 = 1.5625f * d02 * iu;
+        const float rho2 = d02 * iu;
         const float rho6 = rho2 * rho2 * rho2;
         const float rho12 = rho6 * rho6;
         const float eps = ca.y * cj.y;
-        const float qq = ca.w * cj.z;
-        const float e = fmaf(eps, fmaf(-2.0f, rho6, rho12), qq * iu);
-        const float s = on * (fmaf(-12.0f * eps, rho12 - rho6, -2.0f * qq * iu) * iu);
-        ee = fmaf(gj == ga ? 0.0f : (gj < 0 ? 1.0f : 0.5f), e, ee);
+        const float qi = qa * cj.z * iu;
+        const float e = fmaf(eps, fmaf(-2.0f, rho6, rho12), qi);
+        const float s = fmaf(ea12 * cj.y, rho12 - rho6, -2.0f * qi) * (same ? 0.0f : iu);
+        ee = fmaf(same ? 0.0f : cj.w, e, ee);
         fx = fmaf(s, dx, fx);
         fy = fmaf(s, dy, fy);
         fz = fmaf(s, dz, fz);
