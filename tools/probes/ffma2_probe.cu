@@ -1,4 +1,5 @@
 // Throughput probe: scalar FFMA vs packed FFMA2 (fma.rn.f32x2, sm_100a).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/probes/ffma2_probe tools/probes/ffma2_probe.cu
 // Each thread runs 8 independent chains; reports FP32 FLOP/s for both forms.
 #include <cstdio>
 #include <cuda_runtime.h>
