@@ -427,7 +427,11 @@ def run_gpu_arm(args):
                                    "figure)",
                     "flop_per_eval": flop_per_eval(inst, settings.partition),
                     "ls_evals_per_step": ls_evals.value, "ls_kernel_ms_per_launch": ls_ms.value / n_ls_launches,
-                    "traffic": profiled_traffic()}
+                    "traffic": None, "traffic_source": None}
+            tr = profiled_traffic()
+            if tr:  # DRAM bytes per launch from the committed ncu --set full capture
+                roof["traffic"] = tr["bytes_per_launch"]
+                roof["traffic_source"] = f"{tr['source']} (dram__bytes_read.sum + dram__bytes_write.sum, {tr['kernel']})"
             ls_share = ls_ms.value / all_ms.value
 
     if rank == 0:
