@@ -31,6 +31,7 @@ _SIGS = {
     "mdr_ctx_set_warps_per_block": (I, [P, I]),
     "mdr_ctx_set_cta_warps": (I, [P, I]),
     "mdr_ctx_set_exact_torsion": (I, [P, I]),
+    "mdr_site_chunking": (I, [I, I, I, P, P]),
     "mdr_last_error": (C.c_char_p, [P]),
     "mdr_ctx_launch_count": (U64, [P]),
     "mdr_ctx_synchronize": (I, [P]),

@@ -285,6 +285,15 @@ int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
   return MDR_OK;
 }
 
+int mdr_site_chunking(int pair, int na, int ns, int* n_chunks, int* chunk_len) {
+  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || pair < MDR_PAIR_FP64 || pair > MDR_PAIR_FP64_FAST)
+    return fail(nullptr, MDR_ERR_INVALID, "bad argument");
+  *n_chunks = 1;
+  *chunk_len = ns;
+  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, 0, *n_chunks, *chunk_len);
+  return MDR_OK;
+}
+
 int mdr_ctx_set_exact_torsion(mdr_ctx* c, int on) {
   if (!c || (on != 0 && on != 1)) return fail(c, MDR_ERR_INVALID, "exact torsion flag must be 0 or 1");
   c->exact = on;

@@ -30,3 +30,30 @@ def test_python_binding_covers_header():
     declared = set(_lib.exported_symbols()) | set(_lib._OPTIONAL)
     missing = [n for n in header_functions() if n not in declared]
     assert not missing, missing
+
+
+def test_site_chunking_policy():
+    """Host-only policy of the chunked site mapping (capi.cpp pick_chunks):
+    FP64-fast only, chunk lengths a multiple of the 8-site batch, at most 256
+    (atom, chunk) items, lane per atom when chunking does not pay."""
+    from paper_2410_10447_b200 import PAIR_FP32, PAIR_FP64, PAIR_FP64_FAST, build
+
+    lib = ctypes.CDLL(build.build())
+
+    def pick(pair, na, ns):
+        n, ln = ctypes.c_int(), ctypes.c_int()
+        assert lib.mdr_site_chunking(pair, na, ns, ctypes.byref(n), ctypes.byref(ln)) == 0
+        return n.value, ln.value
+
+    assert pick(PAIR_FP64_FAST, 20, 64) == (3, 24)  # C3: measured best (DESIGN §3)
+    assert pick(PAIR_FP64, 20, 64) == (1, 64)
+    assert pick(PAIR_FP32, 20, 64) == (1, 64)
+    assert pick(PAIR_FP64_FAST, 200, 64) == (1, 64)  # items would exceed 256
+    assert pick(PAIR_FP64_FAST, 20, 6) == (1, 6)  # fewer sites than one batch
+    for na in (1, 5, 16, 31, 40, 100, 128):
+        for ns in (8, 30, 64, 200):
+            n, ln = pick(PAIR_FP64_FAST, na, ns)
+            if n > 1:
+                assert ln % 8 == 0 and na * n <= 256 and (n - 1) * ln < ns <= n * ln
+                assert ((na * n + 31) // 32) * (ln + 4) < ((na + 31) // 32) * ns
+    assert lib.mdr_site_chunking(7, 20, 64, ctypes.byref(ctypes.c_int()), ctypes.byref(ctypes.c_int())) != 0
