@@ -421,7 +421,7 @@ def run_gpu_arm(args):
             flops = flop_per_eval(inst, settings.partition) * ls_evals.value
             achieved = flops / (ls_ms.value * 1e-3) / 1e12
             n_ls_launches = settings.generations + 1
-            roof = {"bound": "fp64", "kernel": "lga_ls_kernel (device ADADELTA chain, warp per pose)",
+            roof = {"bound": "fp64", "kernel": "lga_ls_kernel / lga_ls_pair_kernel (device ADADELTA chain, warp (pair) per search)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": "measured live: DFMA-chain kernel on this GPU (MEASURED_PEAKS.json has no FP64 "
                                    "figure)",

@@ -33,7 +33,7 @@ namespace mdr {
 
 // Per-warp shared-memory region: scratch | genotype | best genotype | angle
 // trig table | [exact-torsion torques] | [chunked: positions, chunk sums].
-constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16;
+constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16 + 16;
 
 struct WarpCtx {
   WarpScratch ws;
@@ -54,6 +54,8 @@ __device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, co
   w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
   w.best = w.g + kMaxDim;
   w.ws.trig = reinterpret_cast<double2*>(w.best + kMaxDim);
+  w.ws.ctl = reinterpret_cast<int*>(w.ws.trig + kMaxDim);
+  w.ws.bar = 0;
   unsigned char* q = p + kWarpRegion;
   w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(q) : nullptr;
   if (L.exact_torsion) q += (size_t)16 * L.n_atoms;
@@ -172,7 +174,7 @@ struct LsResult {
 
 // local_search docking.cpp:310-351 run by the calling warp.  start: global
 // or shared genotype.  On return w.best holds the best genotype.
-template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
+template <int METHOD, int PAIR, bool EXACT, int CHUNK>
 __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, int max_iters, double tol,
                                       int partition, bool half_mode, const WarpCtx& w) {
   const int lane = threadIdx.x & 31;
@@ -281,6 +283,8 @@ __device__ __forceinline__ CtaCtx cta_region(unsigned char* base, int n_atoms, i
   c.ws.tq = nullptr;  // exact-torsion mode runs warp per pose only
   c.ws.wpos = c.ws.part = nullptr;
   c.ws.trig = nullptr;
+  c.ws.ctl = nullptr;
+  c.ws.bar = 0;
   c.g = reinterpret_cast<double*>(base + kWarpScratchBytes);
   c.best = c.g + kMaxDim;
   c.part = c.best + kMaxDim;
@@ -585,6 +589,45 @@ __global__ void MDR_LS_BOUNDS lga_ls_kernel(LigandView L, LgaDev D) {
 template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
 __global__ void lga_ls_kernel_nb(LigandView L, LgaDev D) {
   lga_ls_body<METHOD, PAIR, EXACT, CHUNK>(L, D);
+}
+
+// Warp-pair search (FP64-fast, chunked sites): two warps per Lamarckian
+// search; the leader runs local_search_warp<..., CHUNK = 2> and the helper
+// takes half of each evaluation's chunk items (pair_helper).  Same items,
+// same per-item arithmetic, same combine order as the one-warp kernel, so
+// the results are bit-identical; per evaluation two named barriers.
+template <int METHOD>
+__global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SmemLigand S = load_ligand(L, smem);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pose = warp >> 1;
+  const int item = blockIdx.x * (blockDim.x >> 6) + pose;
+  if (item >= D.R * D.L) return;
+  const int run = item / D.L, r = item % D.L;
+  if (!D.active[run]) return;
+  WarpCtx w = warp_region(smem + ligand_smem_bytes(L), pose, L);
+  w.ws.bar = 1 + pose;
+  if (warp & 1) {
+    pair_helper(S, w.ws);
+    return;
+  }
+  const int c = D.cur[run];
+  const int target = ls_target(D, run, r);
+  const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
+  const LsResult res = local_search_warp<METHOD, MDR_PAIR_FP64_FAST, false, 2>(S, start, D.ls_iters, D.tol,
+                                                                              D.partition, D.half_mode != 0, w);
+  if (lane == 0) *w.ws.ctl = 0;
+  pair_bar(w.ws.bar);  // release the helper
+  const size_t o = (size_t)run * D.L + r;
+  for (int d = lane; d < D.dim; d += 32) D.lsg[o * D.dim + d] = w.best[d];
+  if (lane == 0) {
+    D.lse[o] = res.energy;
+    D.lsit[o] = res.iterations;
+    D.lscv[o] = res.converged;
+    D.lstarget[o] = target;
+    if (res.status != MDR_OK) D.status[run] = res.status;
+  }
 }
 
 // First occurrence of the strict minimum of candidate energies e(0..n-1)
@@ -959,6 +1002,32 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
   return cudaGetLastError();
 }
 
+// Warp-pair Lamarckian search (lga_ls_pair_kernel): FP64-fast chunked
+// ligands with more than one wave of chunk items, at most 8 searches per CTA
+// (named barriers 1..8).
+#ifndef MDR_LS_PAIR
+#define MDR_LS_PAIR 1
+#endif
+static bool use_ls_pair(const LigandView& L, int pair, int wpb, int cta_warps) {
+  return MDR_LS_PAIR && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST && L.n_chunks > 1 && !L.exact_torsion &&
+         L.n_atoms * L.n_chunks > 32 && wpb <= 8;
+}
+static cudaError_t prep_ls_pair(int method, size_t smem) {
+  switch (method) {
+    case MDR_METHOD_BASELINE: return prep(lga_ls_pair_kernel<MDR_METHOD_BASELINE>, smem);
+    case MDR_METHOD_TCU: return prep(lga_ls_pair_kernel<MDR_METHOD_TCU>, smem);
+    default: return prep(lga_ls_pair_kernel<MDR_METHOD_TCU_SPLIT>, smem);
+  }
+}
+static void launch_ls_pair(int method, int blocks, int threads, size_t smem, cudaStream_t s, const LigandView& L,
+                           const LgaDev& D) {
+  switch (method) {
+    case MDR_METHOD_BASELINE: lga_ls_pair_kernel<MDR_METHOD_BASELINE><<<blocks, threads, smem, s>>>(L, D); break;
+    case MDR_METHOD_TCU: lga_ls_pair_kernel<MDR_METHOD_TCU><<<blocks, threads, smem, s>>>(L, D); break;
+    default: lga_ls_pair_kernel<MDR_METHOD_TCU_SPLIT><<<blocks, threads, smem, s>>>(L, D); break;
+  }
+}
+
 // Warps of the CTA-per-pose final polish in the fast pair modes (the polish
 // runs one search per LGA run, so its latency, not throughput, counts).
 #ifndef MDR_POLISH_CTA
@@ -976,6 +1045,8 @@ cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int 
   if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, L, smem);
   if (cta_warps > 0) {
     if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
+  } else if (use_ls_pair(L, pair, wpb, cta_warps)) {
+    if (e == cudaSuccess) e = prep_ls_pair(method, smem);
   } else {
     if (e == cudaSuccess) e = prep_lga_ls_kernel(method, pair, L, smem);
   }
@@ -1008,6 +1079,8 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
     if (D.L > 0) {
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
+      else if (use_ls_pair(L, pair, wpb, cta_warps))
+        launch_ls_pair(method, blocks_for((long long)D.R * D.L, wpb), 64 * wpb, smem, s, L, D);
       else
         dispatch_lga_ls_kernel(method, pair, L, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
     }
