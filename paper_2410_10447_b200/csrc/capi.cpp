@@ -54,6 +54,7 @@ struct mdr_ctx {
   int exact = 0;      // analytic mode: exact per-group torsion gradient (mdr_ctx_set_exact_torsion)
   int chunking = 1;   // FP64-fast: chunked site mapping for small ligands (MDR_CHUNKING=0 disables)
   int chunk_len = 0;  // > 0: pin the chunk length (MDR_CHUNK_LEN, timing only)
+  int ls_pair = 1;    // warp-pair Lamarckian searches (MDR_LS_PAIR=0 disables)
 
   std::string err;
   uint64_t launches = 0;
@@ -225,6 +226,7 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   L.exact_torsion = c->exact;
   L.n_chunks = 1;
   L.chunk_len = L.n_sites;
+  L.ls_pair = c->ls_pair;
   if (c->pair == MDR_PAIR_FP64_FAST && c->chunking)
     pick_chunks(L.n_atoms, L.n_sites, c->chunk_len, L.n_chunks, L.chunk_len);
   return L;
@@ -254,6 +256,7 @@ mdr_ctx* mdr_ctx_create(int device) {
   c->stream = c->own;
   if (const char* v = std::getenv("MDR_CHUNKING")) c->chunking = std::atoi(v) != 0;  // A/B timing knobs
   if (const char* v = std::getenv("MDR_CHUNK_LEN")) c->chunk_len = std::atoi(v);
+  if (const char* v = std::getenv("MDR_LS_PAIR")) c->ls_pair = std::atoi(v) != 0;
   return c;
 }
 

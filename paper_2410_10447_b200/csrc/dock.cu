@@ -1009,7 +1009,7 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
 #define MDR_LS_PAIR 1
 #endif
 static bool use_ls_pair(const LigandView& L, int pair, int wpb, int cta_warps) {
-  return MDR_LS_PAIR && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST && L.n_chunks > 1 && !L.exact_torsion &&
+  return MDR_LS_PAIR && L.ls_pair && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST && L.n_chunks > 1 && !L.exact_torsion &&
          L.n_atoms * L.n_chunks > 32 && wpb <= 8;
 }
 static cudaError_t prep_ls_pair(int method, size_t smem) {

@@ -32,6 +32,8 @@ struct LigandView {
   int exact_torsion;  // 1: torsion gradient = exact per-group torque (mdr_ctx_set_exact_torsion)
   int n_chunks;       // FP64-fast: sites split into n_chunks ranges of chunk_len (1 = lane per atom)
   int chunk_len;
+  int ls_pair;        // 1: Lamarckian searches may run on a warp pair (lga_ls_pair_kernel)
+  int pad_;
   const SiteD* sites;
   const double4* atoms;  // local x, y, z, weight
   const int* tors;

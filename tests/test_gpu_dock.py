@@ -313,3 +313,27 @@ def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch
         assert abs(a.energy - b.energy) <= 1e-5 * max(abs(b.energy), 1.0)
     chunked.close()
     lane.close()
+
+
+def test_warp_pair_search_bit_identical(instances, monkeypatch):
+    """FP64-fast chunked ligands run each Lamarckian search on a warp pair
+    (lga_ls_pair_kernel: the helper warp takes half of every evaluation's
+    chunk items).  Same items, same arithmetic, same combine order as the
+    one-warp kernel (MDR_LS_PAIR=0), so whole LGA runs are bit-identical."""
+    from paper_2410_10447_b200.workloads import c3
+
+    pair = Device(0, pair=PAIR_FP64_FAST)
+    monkeypatch.setenv("MDR_LS_PAIR", "0")
+    single = Device(0, pair=PAIR_FP64_FAST)
+    rng = derive_rng(93, "pair/identity")
+    cases = [c3(), random_instance(rng, 3, 28, 64), random_instance(rng, 40, 16, 64)]
+    seeds = np.arange(16, dtype=np.uint64) + np.uint64(4321)
+    for inst in cases:
+        for method in (BASELINE, TCU_SPLIT):
+            a = pair.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
+            b = single.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
+            for x, y in zip(a, b):
+                assert x.best_energy == y.best_energy and x.evaluations == y.evaluations
+                assert np.array_equal(x.best_genotype, y.best_genotype)
+    pair.close()
+    single.close()
