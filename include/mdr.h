@@ -128,8 +128,10 @@ int mdr_ctx_set_exact_torsion(mdr_ctx* ctx, int on);
 /* Site-chunking policy of the warp-per-pose evaluation (host-only, no GPU
  * needed): for FP64-fast pair terms a small ligand's sites are split into
  * *n_chunks ranges of *chunk_len (a multiple of 8) so the n_atoms x n_chunks
- * (atom, chunk) items fill all 32 lanes; *n_chunks = 1 means lane per atom
- * (always the case for the other pair modes).  DESIGN.md §3. */
+ * (atom, chunk) items fill all 32 lanes (64 when the LGA's searches run on a
+ * warp pair, the default context's policy reported here); *n_chunks = 1
+ * means lane per atom (always the case for the other pair modes).
+ * DESIGN.md §3. */
 int mdr_site_chunking(int pair_precision, int n_atoms, int n_sites, int* n_chunks, int* chunk_len);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);

@@ -201,9 +201,13 @@ int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 || c->exac
 // rounds x (len + 4 sites' worth of staging and shorter ILP), with at most
 // kMaxChunkItems items; 1 chunk keeps lane per atom.  C3 (20 atoms x 64
 // sites) measured: lane per atom 145.8, len 8 / 16 / 24 / 32 -> 148.0 /
-// 146.3 / 150.4 / 130.0 M evals/s; the model picks 24.  `force_len` > 0
+// 146.3 / 150.4 / 130.0 M evals/s; the model picks 24.  When the LGA's
+// searches run on a warp pair (`pair_lanes`: more than 32 items go to the
+// 64 lanes of lga_ls_pair_kernel) the rounds are counted over 64 lanes with
+// no staging term, ties to the shorter chunk: C3 measured len 8 / 16 / 24 /
+// 32 -> 170.6 / 162.8 / 165.2 / 142.0 M, the model picks 8.  `force_len` > 0
 // pins len (timing).
-void pick_chunks(int na, int ns, int force_len, int& n_chunks, int& chunk_len) {
+void pick_chunks(int na, int ns, bool pair_lanes, int force_len, int& n_chunks, int& chunk_len) {
   constexpr int kBatch = 8;  // MDR_PV_CHUNK
   n_chunks = 1;
   chunk_len = ns;
@@ -211,7 +215,8 @@ void pick_chunks(int na, int ns, int force_len, int& n_chunks, int& chunk_len) {
   for (int len = kBatch; len < ns; len += kBatch) {
     const int n = (ns + len - 1) / len;
     if (na * n > kMaxChunkItems) continue;
-    const long cost = (long)((na * n + 31) / 32) * (len + 4);
+    const int lanes = pair_lanes && na * n > 32 ? 64 : 32;
+    const long cost = (long)((na * n + lanes - 1) / lanes) * (len + (lanes == 64 ? 0 : 4));
     if (force_len > 0 ? len == force_len : cost < best) {
       best = cost;
       n_chunks = n;
@@ -227,8 +232,9 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   L.n_chunks = 1;
   L.chunk_len = L.n_sites;
   L.ls_pair = c->ls_pair;
+  const bool pair_lanes = c->ls_pair && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
   if (c->pair == MDR_PAIR_FP64_FAST && c->chunking)
-    pick_chunks(L.n_atoms, L.n_sites, c->chunk_len, L.n_chunks, L.chunk_len);
+    pick_chunks(L.n_atoms, L.n_sites, pair_lanes, c->chunk_len, L.n_chunks, L.chunk_len);
   return L;
 }
 
@@ -293,7 +299,7 @@ int mdr_site_chunking(int pair, int na, int ns, int* n_chunks, int* chunk_len) {
     return fail(nullptr, MDR_ERR_INVALID, "bad argument");
   *n_chunks = 1;
   *chunk_len = ns;
-  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, 0, *n_chunks, *chunk_len);
+  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, true, 0, *n_chunks, *chunk_len);
   return MDR_OK;
 }
 

@@ -45,7 +45,7 @@ def test_site_chunking_policy():
         assert lib.mdr_site_chunking(pair, na, ns, ctypes.byref(n), ctypes.byref(ln)) == 0
         return n.value, ln.value
 
-    assert pick(PAIR_FP64_FAST, 20, 64) == (3, 24)  # C3: measured best
+    assert pick(PAIR_FP64_FAST, 20, 64) == (8, 8)  # C3 on the warp-pair search: measured best
     assert pick(PAIR_FP64, 20, 64) == (1, 64)
     assert pick(PAIR_FP32, 20, 64) == (1, 64)
     assert pick(PAIR_FP64_FAST, 200, 64) == (1, 64)  # items would exceed 256
@@ -55,5 +55,6 @@ def test_site_chunking_policy():
             n, ln = pick(PAIR_FP64_FAST, na, ns)
             if n > 1:
                 assert ln % 8 == 0 and na * n <= 256 and (n - 1) * ln < ns <= n * ln
-                assert ((na * n + 31) // 32) * (ln + 4) < ((na + 31) // 32) * ns
+                lanes = 64 if na * n > 32 else 32
+                assert ((na * n + lanes - 1) // lanes) * (ln + (0 if lanes == 64 else 4)) < ((na + 31) // 32) * ns
     assert lib.mdr_site_chunking(7, 20, 64, ctypes.byref(ctypes.c_int()), ctypes.byref(ctypes.c_int())) != 0
