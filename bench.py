@@ -62,6 +62,31 @@ N_ATOMS, N_ROT, N_SITES, N_RUNS = 20, 5, 64, 100
 METHODS = {"baseline": BASELINE, "tcu": TCU, "split": TCU_SPLIT}
 
 
+def run_seeds(rank: int) -> np.ndarray:
+    """The seeds rank `rank` docks each step (both arms): 1 000 000 + 100 r + i,
+    validate_pair-style base + offset (reference docking.cpp:558-564)."""
+    return np.arange(N_RUNS, dtype=np.uint64) + np.uint64(1_000_000 + rank * N_RUNS)
+
+
+def bench_config(world: int) -> dict:
+    """The workload both arms report (identical dicts)."""
+    return {"workload": "C3 small-ligand docking: 100 LGA runs per GPU (BASELINE.json configs[2])",
+            "n_atoms": N_ATOMS, "n_rot": N_ROT, "n_sites": N_SITES, "runs_per_gpu": N_RUNS,
+            "seeds": "1000000 + 100*rank + i, i < 100", "lga": "default LgaSettings (pop 36, 20 gens, LS 150 iters, "
+            "partition 64)", "parallelism": f"runs sharded x{world}"}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def workload():
     inst = random_instance(derive_rng(12345, "synth/small"), N_ROT, N_ATOMS, N_SITES)
     inst.name = "synth/small"
@@ -171,7 +196,8 @@ def cpu_measure(budget_s=12.0, procs=None):
     if kind == "port" and not available("port"):
         build()
     procs = procs or os.cpu_count() or 1
-    jobs = [([10_000 + p * 1000 + k for k in range(1000)], budget_s, kind) for p in range(procs)]
+    seeds = [int(x) for x in run_seeds(0)]  # the GPU arm's rank-0 seeds, cycled
+    jobs = [([seeds[(p + procs * k) % len(seeds)] for k in range(1000)], budget_s, kind) for p in range(procs)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
@@ -182,8 +208,10 @@ def cpu_measure(budget_s=12.0, procs=None):
     span = max(r[1] for r in res)
     return {"value": evals / span, "unit": UNIT, "cores": procs, "kind": kind,
             "sample": f"{runs} LGA runs of the C3 workload ({N_ATOMS} atoms/{N_ROT} torsions/{N_SITES} sites, "
-                      f"default LgaSettings, Baseline reduction) on {procs} processes x ~{budget_s:.0f} s; "
-                      f"{evals} evaluations", "wall_s": wall}
+                      f"default LgaSettings, Baseline reduction, the GPU arm's seeds 1000000.. cycled) on {procs} "
+                      f"processes x ~{budget_s:.0f} s; {evals} evaluations", "wall_s": wall,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "build": "oracle/_ref: reference sources, g++ -std=c++20 -O3 -DNDEBUG -ffp-contract=off (its Release flags)"}
 
 
 def run_reference_arm(args):
@@ -206,8 +234,7 @@ def run_reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference random_instance recipe)",
-            "config": {"workload": "C3 small-ligand docking, 100 LGA runs", "n_atoms": N_ATOMS, "n_rot": N_ROT,
-                       "n_sites": N_SITES, "lga": "default LgaSettings", "method": "baseline"},
+            "config": bench_config(args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": last["kind"],
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -322,7 +349,7 @@ def run_gpu_arm(args):
     method = METHODS[args.method]
     accum = SINGLE
     dim = inst.dim
-    seeds_host = np.arange(N_RUNS, dtype=np.uint64) + np.uint64(1_000_000 + rank * N_RUNS)
+    seeds_host = run_seeds(rank)
 
     # device-resident state: instance, seeds, the LGA batch (one CUDA graph)
     dinst = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
@@ -368,8 +395,12 @@ def run_gpu_arm(args):
     t_ms = sum(step_ms)
     t = torch.tensor([t_ms], dtype=torch.float64, device=f"cuda:{local}")
     if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    t_max = float(t.item())
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        rank_ms = [float(x.item()) for x in parts]
+    else:
+        rank_ms = [t_ms]
+    t_max = max(rank_ms)
     total_evals = evals_per_step * args.steps * world
     value = total_evals / (t_max * 1e-3)
 
@@ -444,11 +475,10 @@ def run_gpu_arm(args):
             "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if pair == PAIR_FP32 else "f64",
             "data": "synthetic (reference random_instance recipe, derive_rng(12345,'synth/small'))",
-            "config": {"workload": "C3 small-ligand docking: 100 LGA runs per GPU (BASELINE.json configs[2])",
-                       "n_atoms": N_ATOMS, "n_rot": N_ROT, "n_sites": N_SITES, "runs_per_gpu": N_RUNS,
-                       "lga": "default LgaSettings (pop 36, 20 gens, LS 150 iters, partition 64)",
-                       "reduction": args.method, "pair_terms": args.pair, "parallelism": f"runs sharded x{world}",
-                       "evals_per_step_per_gpu": evals_per_step, "l2": "flushed (256 MB write) before every step"},
+            "config": bench_config(world),
+            "impl_detail": {"reduction": args.method, "pair_terms": args.pair, "evals_per_step_per_gpu": evals_per_step,
+                            "l2": "flushed (256 MB write) before every step",
+                            "rank_ms_per_step": [x / args.steps for x in rank_ms]},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                     "api": "mdr_lga_run_batch (host buffers, synchronous)"},
             "gpu_launches": int(launches),
@@ -715,6 +745,40 @@ def extra_measurements(args, dev, lib, torch):
     return out
 
 
+def launch_plan(gpus: int, env, device_count: int, impl: str = "b200"):
+    """How `bench.py --gpus N` runs: ("rank", W) when already one rank of a
+    torchrun job of W processes (W must equal N), ("direct", 1) for N = 1,
+    ("spawn", N) to re-launch itself as N ranks (one process per GPU).
+    Raises when the request cannot be met (never silently runs on fewer GPUs)."""
+    if gpus < 1:
+        raise SystemExit(f"--gpus must be >= 1 (got {gpus})")
+    if "WORLD_SIZE" in env:
+        world = int(env["WORLD_SIZE"])
+        if world != gpus:
+            raise SystemExit(f"--gpus {gpus} but this torchrun job has WORLD_SIZE={world}")
+        if impl == "b200" and device_count < world:
+            raise SystemExit(f"WORLD_SIZE={world} ranks but only {device_count} visible GPU(s)")
+        return ("rank", world)
+    if gpus == 1 or impl != "b200":  # the CPU reference arm runs once, on the host
+        return ("direct", 1)
+    if device_count < gpus:
+        raise SystemExit(f"--gpus {gpus} requested but only {device_count} visible GPU(s)")
+    return ("spawn", gpus)
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-run this script as n ranks (torch.distributed.run, one process
+    per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -731,6 +795,15 @@ def main():
     ap.add_argument("--extra", action="store_true", default=True)
     ap.add_argument("--no-extra", dest="extra", action="store_false")
     args = ap.parse_args()
+    if args.impl == "b200":
+        import torch
+
+        ndev = torch.cuda.device_count()
+    else:
+        ndev = 0
+    mode, _ = launch_plan(args.gpus, os.environ, ndev, args.impl)
+    if mode == "spawn":
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

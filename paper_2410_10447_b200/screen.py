@@ -13,7 +13,10 @@ RMSD clustering on the device).
     block_syncs,atomic_adds,mma_ops`, %.17g numbers, RFC-4180 quoting), one
     row per docking run, appended after every batch;
   * resume: ligands whose every run already has a row are skipped
-    (keyed on (instance, seed));
+    (keyed on (instance, seed)); a crash can leave at most a partial last
+    line, which the loader drops (and trims from the file) before appending;
+    with world > 1 every rank writes its own file `<csv_path>.rank<r>`, so
+    ranks never interleave lines;
   * gather: the only collective — every rank's rows to rank 0
     (torch.distributed.gather_object), which writes the merged CSV ordered
     by (instance, seed).
@@ -111,6 +114,39 @@ def parse_results(text: str):
     return rows
 
 
+def load_done_rows(path: str):
+    """Rows of a results CSV being resumed.  Repeated header lines are
+    skipped and a trailing partial record (no final newline, or a bad field
+    count on the last line — a crash mid-append) is dropped and trimmed from
+    the file, so the next append starts on a clean line.  Damage anywhere
+    else still raises (parse_results)."""
+    with open(path) as f:
+        text = f.read()
+    lines = text.split("\n")
+    tail = lines.pop()  # "" when the file ends with a newline
+    if tail:
+        text = text[: len(text) - len(tail)]
+    if lines and lines[-1] != HEADER and len(_split(lines[-1])) != 10:
+        text = text[: len(text) - len(lines[-1]) - 1]
+        lines.pop()
+    if len(text) != os.path.getsize(path):
+        tmp = path + ".tmp"
+        with open(tmp, "w") as f:
+            f.write(text)
+        os.replace(tmp, path)
+    body = [ln for i, ln in enumerate(lines) if ln and not (ln == HEADER and i > 0)]
+    return parse_results("\n".join(body) + "\n") if body else []
+
+
+def _append(path: str, block: str):
+    """One write + fsync per batch: a crash loses at most the last batch's
+    tail, which load_done_rows trims."""
+    with open(path, "a") as f:
+        f.write(block)
+        f.flush()
+        os.fsync(f.fileno())
+
+
 def run_seed(base_seed: int, ligand: int, run: int, runs: int) -> int:
     """Seed of run k of ligand j (validate_pair-style base + offset,
     reference docking.cpp:562)."""
@@ -150,14 +186,14 @@ def screen(dev, dgrid, ligand_fn, n_ligands: int, runs: int, settings, method: i
     names = names or [f"synth/lig/{j}" for j in range(n_ligands)]
     mine = shard(n_ligands, rank, world)
     done = set()
+    if csv_path and world > 1:
+        csv_path = f"{csv_path}.rank{rank}"
     if csv_path and os.path.exists(csv_path):
-        with open(csv_path) as f:
-            done = {(r.instance, r.seed) for r in parse_results(f.read())}
+        done = {(r.instance, r.seed) for r in load_done_rows(csv_path)}
     todo = pending(mine, names, runs, base_seed, done)
     rows, clusters = [], {}
-    if csv_path and not os.path.exists(csv_path):
-        with open(csv_path, "w") as f:
-            f.write(HEADER + "\n")
+    if csv_path and (not os.path.exists(csv_path) or os.path.getsize(csv_path) == 0):
+        _append(csv_path, HEADER + "\n")
     mname = METHOD_NAMES[method]
     for b0 in range(0, len(todo), batch):
         ids = todo[b0:b0 + batch]
@@ -174,8 +210,7 @@ def screen(dev, dgrid, ligand_fn, n_ligands: int, runs: int, settings, method: i
             clusters[names[j]] = (r["cluster_of"].tolist(), r["n_clusters"])
         rows += new
         if csv_path:
-            with open(csv_path, "a") as f:
-                f.write(write_results(new).split("\n", 1)[1])
+            _append(csv_path, write_results(new).split("\n", 1)[1])
     return rows, clusters
 
 

@@ -32,10 +32,14 @@ class RunResult:
 
 
 def pack_results(results, dim: int) -> np.ndarray:
-    """Flatten RunResults into one float64 array: [seed, E, evals, conv, g...]."""
+    """Flatten RunResults into one float64 array: [seed, E, evals, conv, g...].
+    The seed column holds the uint64 seed's BITS (viewed as float64, never
+    converted), so every seed the reference accepts (any uint64, cli.cpp
+    --seed) survives the gather exactly; sorting uses the uint64 view."""
     out = np.zeros((len(results), 4 + dim), np.float64)
+    seeds = np.array([int(r.seed) for r in results], dtype=np.uint64)
+    out[:, 0] = seeds.view(np.float64)
     for k, r in enumerate(results):
-        out[k, 0] = float(r.seed)
         out[k, 1] = r.best_energy
         out[k, 2] = float(r.evaluations)
         out[k, 3] = 1.0 if r.converged else 0.0
@@ -43,8 +47,19 @@ def pack_results(results, dim: int) -> np.ndarray:
     return out
 
 
+def seed_column(arr: np.ndarray) -> np.ndarray:
+    """The uint64 seeds of packed rows (bit view of column 0)."""
+    return np.ascontiguousarray(arr[:, 0]).view(np.uint64)
+
+
+def sort_by_seed(arr: np.ndarray) -> np.ndarray:
+    return arr[np.argsort(seed_column(arr), kind="stable")]
+
+
 def unpack_results(arr: np.ndarray):
-    return [RunResult(int(row[0]), float(row[1]), int(row[2]), bool(row[3]), row[4:].copy()) for row in arr]
+    seeds = seed_column(arr) if len(arr) else np.zeros(0, np.uint64)
+    return [RunResult(int(sd), float(row[1]), int(row[2]), bool(row[3]), row[4:].copy())
+            for sd, row in zip(seeds, arr)]
 
 
 def gather_to_rank0(local: np.ndarray, dist, device=None):
@@ -67,7 +82,7 @@ def gather_to_rank0(local: np.ndarray, dist, device=None):
     if dist.get_rank() != 0:
         return None
     rows = np.concatenate([b[: int(s.item())].cpu().numpy() for b, s in zip(bufs, sizes)], axis=0)
-    return rows[np.argsort(rows[:, 0], kind="stable")]
+    return sort_by_seed(rows)
 
 
 def dock_sharded(inst, seeds, method, accum, settings, dist=None, device=None, dock_fn=None):
@@ -90,7 +105,7 @@ def dock_sharded(inst, seeds, method, accum, settings, dist=None, device=None, d
     local = dock_fn(inst, method, accum, settings, mine) if mine.size else []
     packed = pack_results(local, inst.dim)
     if dist is None:
-        return unpack_results(packed[np.argsort(packed[:, 0], kind="stable")])
+        return unpack_results(sort_by_seed(packed))
     rows = gather_to_rank0(packed, dist, device)
     return None if rows is None else unpack_results(rows)
 

@@ -100,6 +100,46 @@ def test_screen_resume_skips_done():
         assert sorted(got, key=lambda r: (r.instance, r.seed)) == sc.gather_rows(rows1 + rows2, 0, 1)
 
 
+def test_screen_resume_after_partial_line_and_repeated_header():
+    """A crash mid-append leaves a partial last record; a concatenated file
+    can carry a second header.  Resume must drop the partial record (and
+    redo that run), skip the header, and leave a file parse_results reads."""
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "res.csv")
+        s = LgaSettings(partition=64)
+        rows1, _ = sc.screen(FakeDev(), None, _lig, 4, 3, s, batch=2, csv_path=path)
+        with open(path) as f:
+            text = f.read()
+        lines = text.splitlines()
+        # drop the last full record, append its first half without newline
+        broken = "\n".join(lines[:-1]) + "\n" + sc.HEADER + "\n" + lines[-1][: len(lines[-1]) // 2]
+        with open(path, "w") as f:
+            f.write(broken)
+        rows2, _ = sc.screen(FakeDev(), None, _lig, 4, 3, s, batch=2, csv_path=path)
+        assert len(rows2) == 3  # ligand 3 (whose last run was torn) is redone
+        with open(path) as f:
+            body = [ln for i, ln in enumerate(f.read().splitlines()) if not (ln == sc.HEADER and i > 0)]
+        got = sc.parse_results("\n".join(body) + "\n")
+        keys = sorted((r.instance, r.seed) for r in got)
+        assert len(set(keys)) == 12 and len(keys) == 14  # runs of ligand 3 written twice, once torn-free
+        rows3, _ = sc.screen(FakeDev(), None, _lig, 4, 3, s, batch=2, csv_path=path)
+        assert rows3 == []
+
+
+def test_screen_ranks_write_separate_files():
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "res.csv")
+        s = LgaSettings(partition=64)
+        for r in range(2):
+            sc.screen(FakeDev(), None, _lig, 5, 2, s, batch=2, csv_path=path, rank=r, world=2)
+        assert not os.path.exists(path)
+        n = 0
+        for r in range(2):
+            with open(f"{path}.rank{r}") as f:
+                n += len(sc.parse_results(f.read()))
+        assert n == 10
+
+
 def _worker(rank, world, port, out):
     import torch.distributed as dist
 

@@ -86,3 +86,57 @@ def test_dock_sharded_gloo_world2_matches_single_process(instances):
         assert g[1] == w.best_energy and g[2] == w.evaluations and g[3] == w.converged
         assert g[4] == w.best_genotype.tolist()
     assert best_pose(want).best_energy == min(w.best_energy for w in want)
+
+
+BIG_SEEDS = np.array([2**63 + 5, 2**63 + 4, 500, 2**64 - 1, 2**53 + 1, 2**53, 7], dtype=np.uint64)
+
+
+def _fake_dock(inst, method, accum, settings, seeds):
+    """Deterministic per-seed stand-in (tests the packing/gather only)."""
+    return [RunResult(int(s), -float(int(s) % 1000), int(s) % 97, bool(int(s) & 1), np.full(inst.dim, float(int(s) % 13)))
+            for s in seeds]
+
+
+def test_pack_unpack_keeps_every_uint64_seed(instances):
+    from paper_2410_10447_b200.shard import pack_results, sort_by_seed, unpack_results
+
+    res = _fake_dock(instances["s1"], None, None, None, BIG_SEEDS)
+    back = unpack_results(sort_by_seed(pack_results(res, instances["s1"].dim)))
+    assert [r.seed for r in back] == sorted(int(s) for s in BIG_SEEDS)
+    assert len({r.seed for r in back}) == BIG_SEEDS.size
+
+
+def _big_worker(rank, world, port, q):
+    import json
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    from paper_2410_10447_b200._abi import Instance
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "instances.json")) as f:
+        raw = json.load(f)["s1"]
+    inst = Instance(np.array(raw["atoms"]), np.array(raw["torsion"]), np.array(raw["sites"]), raw["n_rot"])
+    res = dock_sharded(inst, BIG_SEEDS, None, None, None, dist=dist, dock_fn=_fake_dock)
+    if rank == 0:
+        q.put([(r.seed, r.best_energy, r.evaluations) for r in res])
+    dist.destroy_process_group()
+
+
+def test_gather_world2_keeps_large_seeds():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_big_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [g[0] for g in got] == sorted(int(s) for s in BIG_SEEDS)
+    for sd, e, ev in got:
+        assert e == -float(sd % 1000) and ev == sd % 97
