@@ -438,6 +438,15 @@ int mdr_cluster_segments_dev(mdr_ctx* ctx, const mdr_dev_instance* dinst, const 
 int mdr_lga_batch_cluster(mdr_ctx* ctx, mdr_lga_batch* b, double rmsd_tol, int32_t* cluster_of,
                           double* rmsd_to_seed, int32_t* n_clusters);
 
+/* Diagnostics: clock64 phase counters of the warp-pair Lamarckian search,
+ * summed over all searches since the last reset (16 x uint64: leader phases
+ * 0 ADADELTA, 1 trig+frame+positions, 2 barrier B1, 3 chunk items, 4 barrier
+ * B2, 5 chunk combine + reduction, 6 projection + best/history; [7]
+ * evaluations; helper 8 wait B1, 9 items, 10 wait B2; [11] searches).  Only
+ * an experiment build with -DMDR_PHASE_PROF=1 records them; the product
+ * build returns MDR_ERR_INVALID. */
+int mdr_phase_prof(uint64_t* out16, int reset);
+
 #ifdef __cplusplus
 }
 #endif

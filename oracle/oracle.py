@@ -286,3 +286,23 @@ class Oracle:
         nc = C.c_int32()
         self._chk(f(inst.cref(), dptr(g), dptr(e), n, rmsd_tol, c.ctypes.data, dptr(r), C.byref(nc)))
         return c, r, nc.value
+
+
+def _lga_job(args):
+    kind, inst, method, accum, settings, seed = args
+    r = Oracle(kind).lga_run(inst, method, accum, settings, int(seed))
+    return r["best_energy"], r["evaluations"], r["converged"], np.asarray(r["best_genotype"]).copy()
+
+
+def lga_runs_parallel(kind, inst, method, accum, settings: LgaSettings, seeds, procs=None):
+    """Test infrastructure: CPU LGA runs (one per seed) on a pool of
+    `spawn`ed processes (safe after CUDA initialisation in the parent, and
+    processes rather than threads: the reference's per-call vectors contend
+    on the allocator).  Returns a list of (best_energy,
+    evaluations, converged, best_genotype) in seed order."""
+    import multiprocessing as mp
+
+    procs = procs or min(len(seeds), os.cpu_count() or 1)
+    jobs = [(kind, inst, method, accum, settings, int(s)) for s in seeds]
+    with mp.get_context("spawn").Pool(procs) as pool:
+        return pool.map(_lga_job, jobs)

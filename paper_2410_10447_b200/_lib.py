@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmdr_b200.so")
+# MDR_LIB_PATH selects an experiment build (variants/<name>/, see build.py)
+LIB_PATH = os.environ.get("MDR_LIB_PATH") or os.path.join(HERE, "libmdr_b200.so")
 
 _lib = None
 
@@ -23,6 +24,7 @@ SZ = C.c_size_t
 # name -> (restype, argtypes)
 _SIGS = {
     "mdr_version": (C.c_char_p, []),
+    "mdr_phase_prof": (I, [P, I]),
     "mdr_ctx_create": (P, [I]),
     "mdr_ctx_destroy": (None, [P]),
     "mdr_ctx_set_stream": (I, [P, P]),

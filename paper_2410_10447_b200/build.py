@@ -37,20 +37,24 @@ def _deps():
     return files
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, defines=()) -> str:
+    """Build the product library, or (variant = name, defines = ["-DX=1", ...])
+    an experiment build into variants/<name>/libmdr_b200.so (A/B timing and
+    instrumented runs; loaded with MDR_LIB_PATH, never by default)."""
+    lib = LIB if variant is None else os.path.join(HERE, "variants", variant, "libmdr_b200.so")
+    if not force and up_to_date(lib):
+        return lib
+    objdir = os.path.join(HERE, "build" if variant is None else os.path.join("variants", variant, "build"))
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-lineinfo", "-std=c++17", "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
-              f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("MDR_NVCC_EXTRA", "").split()  # experiments only
+              f"-I{INCLUDE}", f"-I{CSRC}"] + list(defines) + os.environ.get("MDR_NVCC_EXTRA", "").split()
     objs, procs = [], []
     headers = [f for f in _deps() if f not in sources()]
     flags_file = os.path.join(objdir, "flags.txt")
@@ -68,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [NVCC, *ARCH, *common, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
         else:  # host-only C++ (C-ABI, drop-in C++ API): g++, C++20, no FP contraction
             cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
-                   f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include", "-c", src, "-o", obj]
+                   f"-I{INCLUDE}", f"-I{CSRC}", "-I/usr/local/cuda/include", *defines, "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
     for src, p in procs:
         out, _ = p.communicate()
@@ -78,13 +82,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(out)
     with open(flags_file, "w") as f:
         f.write(flags)
-    link = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-Xcompiler", "-pthread", "-o", LIB, *objs,
+    link = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-Xcompiler", "-pthread", "-o", lib, *objs,
             "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     p = subprocess.run(link, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError("link failed:\n" + p.stdout + p.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2410_10447_b200.build [--force] [-v] [--variant NAME -DX=1 ...]
+    argv = sys.argv[1:]
+    var = argv[argv.index("--variant") + 1] if "--variant" in argv else None
+    print(build(force="--force" in argv, verbose="-v" in argv, variant=var,
+                defines=[a for a in argv if a.startswith("-D")]))

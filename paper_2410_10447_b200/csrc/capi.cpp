@@ -251,6 +251,15 @@ extern "C" {
 
 const char* mdr_version(void) { return "mdr-b200 0.1.0 (sm_100a)"; }
 
+int mdr_phase_prof(uint64_t* out16, int reset) {
+  if (!out16) return fail(nullptr, MDR_ERR_INVALID, "null argument");
+  unsigned long long v[16];
+  if (!phase_prof_read(v, reset != 0))
+    return fail(nullptr, MDR_ERR_INVALID, "not a phase-profiling build (-DMDR_PHASE_PROF=1)");
+  for (int k = 0; k < 16; ++k) out16[k] = v[k];
+  return MDR_OK;
+}
+
 mdr_ctx* mdr_ctx_create(int device) {
   if (cudaSetDevice(device) != cudaSuccess) return nullptr;
   mdr_ctx* c = new mdr_ctx;

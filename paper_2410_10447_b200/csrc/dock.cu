@@ -17,6 +17,10 @@
 
 namespace mdr {
 
+#if MDR_PHASE_PROF
+__device__ unsigned long long g_phase[16];
+#endif
+
 // Register-allocation hint for the warp-per-pose search kernels (at most 16
 // warps per CTA).  Without it ptxas gives the chunked-site variant 100
 // registers and a 2-site-deep schedule (117 M evals/s on C3); with it, 128
@@ -33,7 +37,7 @@ namespace mdr {
 
 // Per-warp shared-memory region: scratch | genotype | best genotype | angle
 // trig table | [exact-torsion torques] | [chunked: positions, chunk sums].
-constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16 + 16;
+constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16 + 16 + (MDR_PHASE_PROF ? 128 : 0);
 
 struct WarpCtx {
   WarpScratch ws;
@@ -56,6 +60,7 @@ __device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, co
   w.ws.trig = reinterpret_cast<double2*>(w.best + kMaxDim);
   w.ws.ctl = reinterpret_cast<int*>(w.ws.trig + kMaxDim);
   w.ws.bar = 0;
+  w.ws.prof = MDR_PHASE_PROF ? reinterpret_cast<long long*>(w.ws.ctl + 4) : nullptr;
   unsigned char* q = p + kWarpRegion;
   w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(q) : nullptr;
   if (L.exact_torsion) q += (size_t)16 * L.n_atoms;
@@ -215,6 +220,7 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
       w.g[lane + 32] = x;
     }
     __syncwarp();
+    if (CHUNK == 2) prof_mark(w.ws, 0);
     o = score_sums<METHOD, PAIR, EXACT, CHUNK>(S, w.g, partition, half_mode, w.ws, f);
     gr0 = lane < dim ? project_dim<EXACT>(S, f, o, lane, w.ws) : 0.f;
     gr1 = lane + 32 < dim ? project_dim<EXACT>(S, f, o, lane + 32, w.ws) : 0.f;
@@ -226,6 +232,7 @@ __device__ LsResult local_search_warp(const SmemLigand& S, const double* start, 
     const double old = __shfl_sync(kFull, hist, slot);  // best_history[iter - 16]
     if (lane == slot) hist = r.energy;
     r.iterations = iter;
+    if (CHUNK == 2) prof_mark(w.ws, 6);
     if (iter >= kWindow && old - r.energy < tol) {
       r.converged = 1;
       break;
@@ -608,10 +615,37 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
   if (!D.active[run]) return;
   WarpCtx w = warp_region(smem + ligand_smem_bytes(L), pose, L);
   w.ws.bar = 1 + pose;
+#if MDR_PHASE_PROF
+  // leader: phases 0-6 (+ [7] evaluations); helper: 8-10 (own slots)
+  if (lane == 0) {
+    if (!(warp & 1))
+      for (int k = 0; k < 16; ++k) w.ws.prof[k] = 0;
+  }
+  pair_bar(w.ws.bar);
+  if (lane == 0) w.ws.prof[(warp & 1) ? 14 : 15] = clock64();
+  pair_bar(w.ws.bar);
+  if (warp & 1) {
+    // the helper keeps its own last stamp in slot 14
+    long long* pf = w.ws.prof;
+    for (;;) {
+      pair_bar(w.ws.bar);
+      if (lane == 0) { const long long t = clock64(); pf[8] += t - pf[14]; pf[14] = t; }
+      if (*w.ws.ctl == 0) break;
+      fast_sums_items(S, w.ws, 32 + lane, 64);
+      if (lane == 0) { const long long t = clock64(); pf[9] += t - pf[14]; pf[14] = t; }
+      pair_bar(w.ws.bar);
+      if (lane == 0) { const long long t = clock64(); pf[10] += t - pf[14]; pf[14] = t; }
+    }
+    if (lane == 0)
+      for (int k = 8; k <= 10; ++k) atomicAdd(&g_phase[k], (unsigned long long)pf[k]);
+    return;
+  }
+#else
   if (warp & 1) {
     pair_helper(S, w.ws);
     return;
   }
+#endif
   const int c = D.cur[run];
   const int target = ls_target(D, run, r);
   const double* start = D.pop[c ^ 1] + ((size_t)run * D.P + target) * D.dim;
@@ -619,6 +653,13 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
                                                                               D.partition, D.half_mode != 0, w);
   if (lane == 0) *w.ws.ctl = 0;
   pair_bar(w.ws.bar);  // release the helper
+#if MDR_PHASE_PROF
+  if (lane == 0) {
+    for (int k = 0; k <= 6; ++k) atomicAdd(&g_phase[k], (unsigned long long)w.ws.prof[k]);
+    atomicAdd(&g_phase[7], (unsigned long long)(res.iterations + 1));
+    atomicAdd(&g_phase[11], 1ull);
+  }
+#endif
   const size_t o = (size_t)run * D.L + r;
   for (int d = lane; d < D.dim; d += 32) D.lsg[o * D.dim + d] = w.best[d];
   if (lane == 0) {
@@ -1138,6 +1179,22 @@ cudaError_t launch_lga_gen_finalize(const LgaDev& D, int gen, cudaStream_t s) {
 cudaError_t launch_lga_total(const LgaDev& D, long long* out, cudaStream_t s) {
   lga_total_evals<<<1, 256, 0, s>>>(D, out);
   return cudaGetLastError();
+}
+
+// Phase-profile counters of an MDR_PHASE_PROF build (false otherwise).
+bool phase_prof_read(unsigned long long* out16, bool reset) {
+#if MDR_PHASE_PROF
+  if (cudaMemcpyFromSymbol(out16, g_phase, sizeof(unsigned long long) * 16) != cudaSuccess) return false;
+  if (reset) {
+    unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(g_phase, z, sizeof(z)) != cudaSuccess) return false;
+  }
+  return true;
+#else
+  (void)out16;
+  (void)reset;
+  return false;
+#endif
 }
 
 }  // namespace mdr

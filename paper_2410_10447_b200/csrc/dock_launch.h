@@ -60,6 +60,7 @@ cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int 
                            cudaStream_t s);
 
 cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s);
+bool phase_prof_read(unsigned long long* out16, bool reset);
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 
 // bench_reduce.cu (C2 microbench)
