@@ -128,11 +128,18 @@ int mdr_ctx_set_exact_torsion(mdr_ctx* ctx, int on);
 /* Site-chunking policy of the warp-per-pose evaluation (host-only, no GPU
  * needed): for FP64-fast pair terms a small ligand's sites are split into
  * *n_chunks ranges of *chunk_len (a multiple of 8) so the n_atoms x n_chunks
- * (atom, chunk) items fill all 32 lanes (64 when the LGA's searches run on a
- * warp pair, the default context's policy reported here); *n_chunks = 1
- * means lane per atom (always the case for the other pair modes).
- * DESIGN.md §3. */
+ * (atom, chunk) items fill all 32 lanes of the warp-per-pose kernels (score,
+ * LGA init / offspring, one-warp search, polish); *n_chunks = 1 means lane
+ * per atom (always the case for the other pair modes).  DESIGN.md §3. */
 int mdr_site_chunking(int pair_precision, int n_atoms, int n_sites, int* n_chunks, int* chunk_len);
+/* The same policy for the LGA's Lamarckian search on `warps` warps per
+ * search (its items spread over 32 * warps lanes; the default context runs
+ * 2, mdr_ctx_set_ls_warps). */
+int mdr_search_chunking(int pair_precision, int n_atoms, int n_sites, int warps, int* n_chunks, int* chunk_len);
+/* Warps per Lamarckian search of the LGA (default 2; 1 = one warp per
+ * search, 0 = the legacy warp-pair kernel; env MDR_LS_WARPS).  Every choice
+ * gives bit-identical results for the same chunking. */
+int mdr_ctx_set_ls_warps(mdr_ctx* ctx, int warps);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);
 /* Number of kernel launches this context has enqueued so far. */
@@ -160,6 +167,13 @@ int mdr_mma_batch(mdr_ctx* ctx, const uint16_t* a, const uint16_t* b,
  * stats = SyncStats of ONE reduction as the reference counts it. */
 int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red,
                       int method, int accum, float* out, mdr_sync_stats* stats);
+/* Device-pointer form of mdr_reduce4_batch (enqueue on the context's stream,
+ * no copies, no sync).  TCU_SPLIT batches of n % 32 == 0 records and at
+ * least 148*32 reductions run as one batched tcgen05 contraction (tf32 hi/lo,
+ * 32 reductions per 128-row tile, accumulator in TMEM); smaller or ragged
+ * batches run the warp-per-reduction mma.sync kernel.  Same contract. */
+int mdr_reduce4_dev(mdr_ctx* ctx, const float* d_vecs, int n, int n_red,
+                    int method, int accum, float* d_out);
 /* baseline_block_reduce reduce.cpp:136-163, n_red blocks of `threads`. */
 int mdr_block_reduce_batch(mdr_ctx* ctx, const float* values, int threads,
                            int n_red, float* out, mdr_sync_stats* stats);
@@ -169,9 +183,21 @@ int mdr_warp_reduce_batch(mdr_ctx* ctx, const float* lanes, int n_red,
 /* reduce7 reduce.cpp:165-209.  recs: n_red x n x {e,gx,gy,gz,tx,ty,tz}. */
 int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red,
                       int method, int accum, float* out, mdr_sync_stats* stats);
+/* Device-pointer form of mdr_reduce7_batch; TCU_SPLIT batches route to the
+ * tcgen05 contraction as in mdr_reduce4_dev (16 reductions x 8 rows per
+ * tile). */
+int mdr_reduce7_dev(mdr_ctx* ctx, const float* d_recs, int n, int n_red,
+                    int method, int accum, float* d_out);
+/* 1 when a TCU_SPLIT reduce4/reduce7 call of this shape runs on tcgen05. */
+int mdr_reduce_uses_tc05(mdr_ctx* ctx, int method, int n, int n_red);
+/* Route TCU_SPLIT batches to tcgen05 (default 1; env MDR_TC05=0). */
+int mdr_ctx_set_tc05(mdr_ctx* ctx, int on);
 
 /* Self test: bit mismatches of the branch-free FP64 division of the strict
  * pair loop against IEEE div.rn.f64 over n counter-generated operand pairs. */
+/* Self test: bit mismatches of the branch-free FP64 square root of the LGA
+ * search against IEEE sqrt.rn.f64 over n counter-generated arguments. */
+int mdr_selftest_dsqrt(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
 int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
 /* Self test: the device's correctly rounded sin, cos (angles in [-pi, pi)),
  * log (Box-Muller u1) and cos(2 pi u2) (crmath.cuh), then CUDA libdevice's,

@@ -34,6 +34,8 @@ _SIGS = {
     "mdr_ctx_set_cta_warps": (I, [P, I]),
     "mdr_ctx_set_exact_torsion": (I, [P, I]),
     "mdr_site_chunking": (I, [I, I, I, P, P]),
+    "mdr_search_chunking": (I, [I, I, I, I, P, P]),
+    "mdr_ctx_set_ls_warps": (I, [P, I]),
     "mdr_last_error": (C.c_char_p, [P]),
     "mdr_ctx_launch_count": (U64, [P]),
     "mdr_ctx_synchronize": (I, [P]),
@@ -44,6 +46,10 @@ _SIGS = {
     "mdr_block_reduce_batch": (I, [P, P, I, I, P, P]),
     "mdr_warp_reduce_batch": (I, [P, P, I, P, P]),
     "mdr_reduce7_batch": (I, [P, P, I, I, I, I, P, P]),
+    "mdr_reduce4_dev": (I, [P, P, I, I, I, I, P]),
+    "mdr_reduce7_dev": (I, [P, P, I, I, I, I, P]),
+    "mdr_reduce_uses_tc05": (I, [P, I, I, I]),
+    "mdr_ctx_set_tc05": (I, [P, I]),
     "mdr_score_batch": (I, [P, P, P, I, I, I, I, P, P, P, P]),
     "mdr_score_reference_batch": (I, [P, P, P, I, P, P, P]),
     "mdr_adadelta_step_batch": (I, [P, I, I, D, D, P, P, P, P]),
@@ -62,6 +68,7 @@ _SIGS = {
     "mdr_lga_batch_total_evals_dev": (I, [P, P, P]),
     "mdr_lga_batch_profile_dev": (I, [P, P, P, P, P, P]),
     "mdr_selftest_ddiv": (I, [P, U64, C.c_int64, P]),
+    "mdr_selftest_dsqrt": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_crmath": (I, [P, C.c_int64, P]),
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_reduce_bench_kernels": (I, []),
@@ -90,7 +97,6 @@ _OPTIONAL = {
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
-    "mdr_tc05_reduce4_dev": (I, [P, P, I, I, P]),
 }
 
 

@@ -20,7 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libmdr_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU = ["reduce.cu", "dock.cu", "grid.cu", "cluster.cu", "bench_reduce.cu", "tc05_reduce.cu"]
+CU = ["reduce.cu", "dock.cu", "ls_multi.cu", "grid.cu", "cluster.cu", "bench_reduce.cu", "tc05_reduce.cu"]
 CPP = ["capi.cpp", "dropin.cpp", "multi.cpp"]
 
 

@@ -55,6 +55,9 @@ struct mdr_ctx {
   int chunking = 1;   // FP64-fast: chunked site mapping for small ligands (MDR_CHUNKING=0 disables)
   int chunk_len = 0;  // > 0: pin the chunk length (MDR_CHUNK_LEN, timing only)
   int ls_pair = 1;    // warp-pair Lamarckian searches (MDR_LS_PAIR=0 disables)
+  int tc05 = 1;       // TcuSplit batched reductions on tcgen05 where they win (MDR_TC05=0 disables)
+  int ls_warps = 2;   // warps per LGA Lamarckian search (ls_multi.cu; MDR_LS_WARPS, 0 = legacy pair kernel)
+  int ls_chunk_len = 0;  // > 0: pin the search's chunk length (MDR_LS_CHUNK_LEN, timing only)
 
   std::string err;
   uint64_t launches = 0;
@@ -207,7 +210,7 @@ int cta_warps_for(const mdr_ctx* c) { return c->pair == MDR_PAIR_FP64 || c->exac
 // no staging term, ties to the shorter chunk: C3 measured len 8 / 16 / 24 /
 // 32 -> 170.6 / 162.8 / 165.2 / 142.0 M, the model picks 8.  `force_len` > 0
 // pins len (timing).
-void pick_chunks(int na, int ns, bool pair_lanes, int force_len, int& n_chunks, int& chunk_len) {
+void pick_chunks(int na, int ns, int search_lanes, int force_len, int& n_chunks, int& chunk_len) {
   constexpr int kBatch = 8;  // MDR_PV_CHUNK
   n_chunks = 1;
   chunk_len = ns;
@@ -215,8 +218,8 @@ void pick_chunks(int na, int ns, bool pair_lanes, int force_len, int& n_chunks, 
   for (int len = kBatch; len < ns; len += kBatch) {
     const int n = (ns + len - 1) / len;
     if (na * n > kMaxChunkItems) continue;
-    const int lanes = pair_lanes && na * n > 32 ? 64 : 32;
-    const long cost = (long)((na * n + lanes - 1) / lanes) * (len + (lanes == 64 ? 0 : 4));
+    const int lanes = search_lanes > 32 && na * n > 32 ? search_lanes : 32;
+    const long cost = (long)((na * n + lanes - 1) / lanes) * (len + (lanes > 32 ? 0 : 4));
     if (force_len > 0 ? len == force_len : cost < best) {
       best = cost;
       n_chunks = n;
@@ -232,9 +235,19 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   L.n_chunks = 1;
   L.chunk_len = L.n_sites;
   L.ls_pair = c->ls_pair;
-  const bool pair_lanes = c->ls_pair && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
-  if (c->pair == MDR_PAIR_FP64_FAST && c->chunking)
-    pick_chunks(L.n_atoms, L.n_sites, pair_lanes, c->chunk_len, L.n_chunks, L.chunk_len);
+  L.ls_warps = c->ls_warps;
+  L.ls_n_chunks = 1;
+  L.ls_chunk_len = L.n_sites;
+  // the warp-per-pose kernels (score, init, offspring, one-warp search,
+  // polish) spread chunk items over 32 lanes; the LGA's multi-warp search
+  // over its own 32 * ls_warps (the legacy pair kernel: 64)
+  const bool multi = c->ls_pair && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
+  const int search_lanes = !multi ? 32 : (c->ls_warps >= 2 ? 32 * c->ls_warps : 64);
+  if (c->pair == MDR_PAIR_FP64_FAST && c->chunking) {
+    pick_chunks(L.n_atoms, L.n_sites, 32, c->chunk_len, L.n_chunks, L.chunk_len);
+    pick_chunks(L.n_atoms, L.n_sites, search_lanes, c->ls_chunk_len > 0 ? c->ls_chunk_len : c->chunk_len,
+                L.ls_n_chunks, L.ls_chunk_len);
+  }
   return L;
 }
 
@@ -272,6 +285,9 @@ mdr_ctx* mdr_ctx_create(int device) {
   if (const char* v = std::getenv("MDR_CHUNKING")) c->chunking = std::atoi(v) != 0;  // A/B timing knobs
   if (const char* v = std::getenv("MDR_CHUNK_LEN")) c->chunk_len = std::atoi(v);
   if (const char* v = std::getenv("MDR_LS_PAIR")) c->ls_pair = std::atoi(v) != 0;
+  if (const char* v = std::getenv("MDR_TC05")) c->tc05 = std::atoi(v) != 0;
+  if (const char* v = std::getenv("MDR_LS_WARPS")) c->ls_warps = std::atoi(v);
+  if (const char* v = std::getenv("MDR_LS_CHUNK_LEN")) c->ls_chunk_len = std::atoi(v);
   return c;
 }
 
@@ -303,12 +319,29 @@ int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
   return MDR_OK;
 }
 
+int mdr_ctx_set_ls_warps(mdr_ctx* c, int w) {
+  if (!c || w < 0 || w > 4) return fail(c, MDR_ERR_INVALID, "search warps must be 0..4 (0 = legacy warp pair)");
+  c->ls_warps = w;
+  c->ls_pair = w != 1;
+  return MDR_OK;
+}
+
+int mdr_search_chunking(int pair, int na, int ns, int warps, int* n_chunks, int* chunk_len) {
+  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || warps < 1 || warps > 4 || pair < MDR_PAIR_FP64 ||
+      pair > MDR_PAIR_FP64_FAST)
+    return fail(nullptr, MDR_ERR_INVALID, "bad argument");
+  *n_chunks = 1;
+  *chunk_len = ns;
+  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, 32 * warps, 0, *n_chunks, *chunk_len);
+  return MDR_OK;
+}
+
 int mdr_site_chunking(int pair, int na, int ns, int* n_chunks, int* chunk_len) {
   if (!n_chunks || !chunk_len || na < 0 || ns < 0 || pair < MDR_PAIR_FP64 || pair > MDR_PAIR_FP64_FAST)
     return fail(nullptr, MDR_ERR_INVALID, "bad argument");
   *n_chunks = 1;
   *chunk_len = ns;
-  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, true, 0, *n_chunks, *chunk_len);
+  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, 32, 0, *n_chunks, *chunk_len);
   return MDR_OK;
 }
 
@@ -422,9 +455,16 @@ int mdr_block_reduce_batch(mdr_ctx* ctx, const float* values, int threads, int n
   return MDR_OK;
 }
 
-int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red, int method, int accum, float* out,
-                      mdr_sync_stats* st) {
-  if (!ctx || n_red < 0 || (n_red && (!vecs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+// TcuSplit batches on the tcgen05 contraction (K2t, tc05_reduce.cu): many
+// reductions of a multiple of 32 records, at least kTc05MinRed of them (one
+// 32-reduction tile per CTA on every SM).  Elsewhere the warp-per-reduction
+// mma.sync kernels run.  Both are fp32-accurate (tf32 hi/lo split).
+constexpr int kTc05MinRed = 148 * 32;
+static bool use_tc05(const mdr_ctx* ctx, int method, int n, int n_red) {
+  return ctx->tc05 && method == MDR_METHOD_TCU_SPLIT && n % 32 == 0 && n >= 32 && n_red >= kTc05MinRed;
+}
+
+static int reduce4_check(mdr_ctx* ctx, int n, int method, int accum, mdr_sync_stats* st) {
   if (method < 0 || method > 2) return fail(ctx, MDR_ERR_INVALID, "unknown reduce method");
   if (n < 1) return fail(ctx, MDR_ERR_SIZE, "reduce4 requires at least one vector");
   if (method == MDR_METHOD_BASELINE && !legal_block(n, method))
@@ -440,22 +480,42 @@ int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red, int met
       *st = split_stats(n, 4);
     }
   }
+  return MDR_OK;
+}
+
+static cudaError_t enqueue_reduce4(mdr_ctx* ctx, const float* d_in, int n, int n_red, int method, int accum,
+                                   float* d_out) {
+  if (use_tc05(ctx, method, n, n_red)) return launch_reduce4_tc05(d_in, n, n_red, d_out, 3, S(ctx));
+  return launch_reduce4(d_in, n, n_red, method, accum == MDR_ACCUM_HALF, d_out, S(ctx));
+}
+
+int mdr_reduce4_batch(mdr_ctx* ctx, const float* vecs, int n, int n_red, int method, int accum, float* out,
+                      mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!vecs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = reduce4_check(ctx, n, method, accum, st)) return rc;
   if (n_red == 0) return MDR_OK;
   const size_t cnt = (size_t)n_red * n * 4;
   DevBuf<float> di, dout;
   CK(di.alloc(cnt, S(ctx)));
   CK(dout.alloc((size_t)n_red * 4, S(ctx)));
   CK(cudaMemcpyAsync(di.p, vecs, cnt * 4, cudaMemcpyHostToDevice, S(ctx)));
-  CK(launch_reduce4(di.p, n, n_red, method, accum == MDR_ACCUM_HALF, dout.p, S(ctx)));
+  CK(enqueue_reduce4(ctx, di.p, n, n_red, method, accum, dout.p));
   ctx->launches++;
   CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 16, cudaMemcpyDeviceToHost, S(ctx)));
   CK(cudaStreamSynchronize(S(ctx)));
   return MDR_OK;
 }
 
-int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int method, int accum, float* out,
-                      mdr_sync_stats* st) {
-  if (!ctx || n_red < 0 || (n_red && (!recs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+int mdr_reduce4_dev(mdr_ctx* ctx, const float* d_vecs, int n, int n_red, int method, int accum, float* d_out) {
+  if (!ctx || n_red < 0 || (n_red && (!d_vecs || !d_out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = reduce4_check(ctx, n, method, accum, nullptr)) return rc;
+  if (n_red == 0) return MDR_OK;
+  CK(enqueue_reduce4(ctx, d_vecs, n, n_red, method, accum, d_out));
+  ctx->launches++;
+  return MDR_OK;
+}
+
+static int reduce7_check(mdr_ctx* ctx, int n, int method, int accum, mdr_sync_stats* st) {
   if (method < 0 || method > 2) return fail(ctx, MDR_ERR_INVALID, "unknown reduce method");
   if (method == MDR_METHOD_BASELINE && !legal_block(n, method))
     return fail(ctx, MDR_ERR_BLOCK_SIZE, "baseline_block_reduce supports multiples of 32 in [32, 1024], got " +
@@ -465,16 +525,63 @@ int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int met
                 "tcu reduce7 needs at least 64 records (a full 16x16 tile), got " + std::to_string(n));
   if (method == MDR_METHOD_TCU_SPLIT && n < 1) return fail(ctx, MDR_ERR_SIZE, "reduce7 needs records");
   if (st) *st = reduce7_stats(n, method, accum);
+  return MDR_OK;
+}
+
+static cudaError_t enqueue_reduce7(mdr_ctx* ctx, const float* d_in, int n, int n_red, int method, int accum,
+                                   float* d_out) {
+  if (use_tc05(ctx, method, n, n_red)) return launch_reduce7_tc05(d_in, n, n_red, d_out, 3, S(ctx));
+  return launch_reduce7(d_in, n, n_red, method, accum == MDR_ACCUM_HALF, d_out, S(ctx));
+}
+
+int mdr_reduce7_batch(mdr_ctx* ctx, const float* recs, int n, int n_red, int method, int accum, float* out,
+                      mdr_sync_stats* st) {
+  if (!ctx || n_red < 0 || (n_red && (!recs || !out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = reduce7_check(ctx, n, method, accum, st)) return rc;
   if (n_red == 0) return MDR_OK;
   const size_t cnt = (size_t)n_red * n * 7;
   DevBuf<float> di, dout;
   CK(di.alloc(cnt, S(ctx)));
   CK(dout.alloc((size_t)n_red * 7, S(ctx)));
   CK(cudaMemcpyAsync(di.p, recs, cnt * 4, cudaMemcpyHostToDevice, S(ctx)));
-  CK(launch_reduce7(di.p, n, n_red, method, accum == MDR_ACCUM_HALF, dout.p, S(ctx)));
+  CK(enqueue_reduce7(ctx, di.p, n, n_red, method, accum, dout.p));
   ctx->launches++;
   CK(cudaMemcpyAsync(out, dout.p, (size_t)n_red * 28, cudaMemcpyDeviceToHost, S(ctx)));
   CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
+int mdr_reduce7_dev(mdr_ctx* ctx, const float* d_recs, int n, int n_red, int method, int accum, float* d_out) {
+  if (!ctx || n_red < 0 || (n_red && (!d_recs || !d_out))) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (int rc = reduce7_check(ctx, n, method, accum, nullptr)) return rc;
+  if (n_red == 0) return MDR_OK;
+  CK(enqueue_reduce7(ctx, d_recs, n, n_red, method, accum, d_out));
+  ctx->launches++;
+  return MDR_OK;
+}
+
+int mdr_ctx_set_tc05(mdr_ctx* ctx, int on) {
+  if (!ctx) return MDR_ERR_INVALID;
+  ctx->tc05 = on != 0;
+  return MDR_OK;
+}
+
+int mdr_reduce_uses_tc05(mdr_ctx* ctx, int method, int n, int n_red) {
+  return ctx && use_tc05(ctx, method, n, n_red) ? 1 : 0;
+}
+
+// Self test of the branch-free FP64 square root of the LGA search (ls_multi.cu).
+int mdr_selftest_dsqrt(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches) {
+  if (!ctx || !mismatches || n < 0) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  DevBuf<unsigned long long> d;
+  CK(d.alloc(1, S(ctx)));
+  CK(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), S(ctx)));
+  CK(launch_dsqrt_selftest(seed, (long long)n, d.p, S(ctx)));
+  ctx->launches++;
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  *mismatches = h;
   return MDR_OK;
 }
 
@@ -1185,7 +1292,7 @@ int mdr_lga_run_batch(mdr_ctx* ctx, const mdr_instance* inst, int method, int ac
   if (int rc = check_lga(ctx, method, s)) return rc;
   if (n_runs == 0) return MDR_OK;
   LgaCache& c = ctx->lga;
-  const bool hit = c.b && c.b->cta_warps == cta_warps_for(ctx) && c.b->L.exact_torsion == ctx->exact && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
+  const bool hit = c.b && c.b->cta_warps == cta_warps_for(ctx) && c.b->L.exact_torsion == ctx->exact && c.b->L.ls_warps == ctx->ls_warps && c.b->L.ls_pair == ctx->ls_pair && c.na == inst->n_atoms && c.ns == inst->n_sites && c.nr == inst->n_rot &&
                    c.method == method && c.pair == ctx->pair && c.accum == accum && c.wpb == ctx->wpb &&
                    c.R == n_runs && std::memcmp(&c.s, s, sizeof *s) == 0;
   if (hit) {

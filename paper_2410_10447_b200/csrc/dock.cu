@@ -14,60 +14,13 @@
 #include "dock_launch.h"
 #include "mdr_device.cuh"
 #include "lga_device.cuh"
+#include "warp_region.cuh"
 
 namespace mdr {
 
 #if MDR_PHASE_PROF
 __device__ unsigned long long g_phase[16];
 #endif
-
-// Register-allocation hint for the warp-per-pose search kernels (at most 16
-// warps per CTA).  Without it ptxas gives the chunked-site variant 100
-// registers and a 2-site-deep schedule (117 M evals/s on C3); with it, 128
-// registers and the latency hidden (150 M).  The lane-per-atom variant is
-// unaffected (126 -> 128 registers, same speed).
-#ifndef MDR_LS_LB
-#define MDR_LS_LB 1
-#endif
-#if MDR_LS_LB > 0
-#define MDR_LS_BOUNDS __launch_bounds__(512, MDR_LS_LB)
-#else
-#define MDR_LS_BOUNDS
-#endif
-
-// Per-warp shared-memory region: scratch | genotype | best genotype | angle
-// trig table | [exact-torsion torques] | [chunked: positions, chunk sums].
-constexpr int kWarpRegion = kWarpScratchBytes + 2 * kMaxDim * 8 + kMaxDim * 16 + 16 + (MDR_PHASE_PROF ? 128 : 0);
-
-struct WarpCtx {
-  WarpScratch ws;
-  double* g;
-  double* best;
-};
-
-__host__ __device__ inline size_t warp_region_bytes(const LigandView& L) {
-  return (size_t)kWarpRegion + (L.exact_torsion ? (size_t)16 * L.n_atoms : 0) +
-         (L.n_chunks > 1 ? (size_t)32 * L.n_atoms * (1 + L.n_chunks) : 0);
-}
-
-__device__ __forceinline__ WarpCtx warp_region(unsigned char* base, int warp, const LigandView& L) {
-  unsigned char* p = base + (size_t)warp * warp_region_bytes(L);
-  WarpCtx w;
-  w.ws.tile = reinterpret_cast<__half*>(p);
-  w.ws.rec = reinterpret_cast<float*>(p + 2 * 256 * 2);
-  w.g = reinterpret_cast<double*>(p + kWarpScratchBytes);
-  w.best = w.g + kMaxDim;
-  w.ws.trig = reinterpret_cast<double2*>(w.best + kMaxDim);
-  w.ws.ctl = reinterpret_cast<int*>(w.ws.trig + kMaxDim);
-  w.ws.bar = 0;
-  w.ws.prof = MDR_PHASE_PROF ? reinterpret_cast<long long*>(w.ws.ctl + 4) : nullptr;
-  unsigned char* q = p + kWarpRegion;
-  w.ws.tq = L.exact_torsion ? reinterpret_cast<float4*>(q) : nullptr;
-  if (L.exact_torsion) q += (size_t)16 * L.n_atoms;
-  w.ws.wpos = L.n_chunks > 1 ? reinterpret_cast<double4*>(q) : nullptr;
-  w.ws.part = L.n_chunks > 1 ? reinterpret_cast<double4*>(q) + L.n_atoms : nullptr;
-  return w;
-}
 
 // --------------------------------------------------------------- K3 score
 template <int METHOD, int PAIR, bool EXACT, bool CHUNK>
@@ -606,7 +559,9 @@ __global__ void lga_ls_kernel_nb(LigandView L, LgaDev D) {
 template <int METHOD>
 __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const SmemLigand S = load_ligand(L, smem);
+  SmemLigand S = load_ligand(L, smem);
+  S.nch = L.ls_n_chunks;  // the search's own chunking (64 lanes)
+  S.clen = L.ls_chunk_len;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pose = warp >> 1;
   const int item = blockIdx.x * (blockDim.x >> 6) + pose;
@@ -1050,8 +1005,8 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
 #define MDR_LS_PAIR 1
 #endif
 static bool use_ls_pair(const LigandView& L, int pair, int wpb, int cta_warps) {
-  return MDR_LS_PAIR && L.ls_pair && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST && L.n_chunks > 1 && !L.exact_torsion &&
-         L.n_atoms * L.n_chunks > 32 && wpb <= 8;
+  return MDR_LS_PAIR && L.ls_pair && L.ls_warps != 1 && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST &&
+         L.ls_n_chunks > 1 && !L.exact_torsion && L.n_atoms * L.ls_n_chunks > 32 && wpb <= 8;
 }
 static cudaError_t prep_ls_pair(int method, size_t smem) {
   switch (method) {
@@ -1086,6 +1041,8 @@ cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int 
   if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, L, smem);
   if (cta_warps > 0) {
     if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
+  } else if (ls_multi_supported(L, pair, wpb, cta_warps)) {
+    if (e == cudaSuccess) e = prep_ls_multi(L, method, smem);
   } else if (use_ls_pair(L, pair, wpb, cta_warps)) {
     if (e == cudaSuccess) e = prep_ls_pair(method, smem);
   } else {
@@ -1120,6 +1077,8 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
     if (D.L > 0) {
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
+      else if (ls_multi_supported(L, pair, wpb, cta_warps))
+        launch_ls_multi(L, D, method, wpb, smem, s);
       else if (use_ls_pair(L, pair, wpb, cta_warps))
         launch_ls_pair(method, blocks_for((long long)D.R * D.L, wpb), 64 * wpb, smem, s, L, D);
       else

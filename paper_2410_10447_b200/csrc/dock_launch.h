@@ -62,6 +62,12 @@ cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int 
 cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s);
 bool phase_prof_read(unsigned long long* out16, bool reset);
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
+cudaError_t launch_dsqrt_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
+
+// ls_multi.cu: the LGA's Lamarckian search on L.ls_warps warps per search
+bool ls_multi_supported(const LigandView& L, int pair, int poses, int cta_warps);
+cudaError_t prep_ls_multi(const LigandView& L, int method, size_t smem);
+void launch_ls_multi(const LigandView& L, const LgaDev& D, int method, int poses, size_t smem, cudaStream_t s);
 
 // bench_reduce.cu (C2 microbench)
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
@@ -71,6 +77,8 @@ constexpr int kReduceBenchKernels = 9;  // ids 7, 8 = tcgen05 batched (stream mo
 
 // tc05_reduce.cu: batched float4 reductions, 32 per tcgen05 contraction
 cudaError_t launch_reduce4_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s);
+// the same contraction over Partial7 records (16 reductions x 8 rows per tile)
+cudaError_t launch_reduce7_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s);
 // K2t2: the same contraction fed by TMA bulk copies into a 6-deep ring
 cudaError_t launch_reduce4_tc05_tma(const float* in, int B, int n_red, float* out, cudaStream_t s);
 

@@ -32,8 +32,10 @@ struct LigandView {
   int exact_torsion;  // 1: torsion gradient = exact per-group torque (mdr_ctx_set_exact_torsion)
   int n_chunks;       // FP64-fast: sites split into n_chunks ranges of chunk_len (1 = lane per atom)
   int chunk_len;
-  int ls_pair;        // 1: Lamarckian searches may run on a warp pair (lga_ls_pair_kernel)
-  int pad_;
+  int ls_pair;        // 1: Lamarckian searches may run on several warps (MDR_LS_PAIR=0: one warp)
+  int ls_warps;       // warps per Lamarckian search of the LGA (ls_multi.cu); 1 = the one-warp kernel
+  int ls_n_chunks;    // site chunking of that search (its own lane count), see capi.cpp pick_chunks
+  int ls_chunk_len;
   const SiteD* sites;
   const double4* atoms;  // local x, y, z, weight
   const int* tors;

@@ -129,11 +129,34 @@ __device__ __forceinline__ void load_chunk(const float4* __restrict__ in, int B,
   }
 }
 
+// Partial7 records (reduce7, reduce.cpp:165-209): 16 reductions per tile,
+// 8 rows each (components 0..6 + a zero row).  Warp w stages reductions
+// 4w..4w+3 of the chunk: per reduction 32 records x 7 floats = 224 contiguous
+// floats, lane l takes floats l + 32q (q < 7), one coalesced 128-byte run
+// per step.
+__device__ __forceinline__ void load_chunk7(const float* __restrict__ in, int B, int n_red, int r0, int ch, int warp,
+                                            int lane, float (&xr)[28]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = 4 * warp + j;
+    const float* src = in + ((size_t)(r0 + r) * B + (size_t)ch * kChunk) * 7;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) xr[7 * j + q] = r0 + r < n_red ? __ldcs(src + lane + 32 * q) : 0.f;
+  }
+}
+
+// NC = 4: float4 records, 32 reductions x 4 rows per 128-row tile.
+// NC = 7: Partial7 records, 16 reductions x 8 rows (row 7 stays zero).
+// A row = rows_per_reduction * r + c sits in the K-major core-matrix layout
+// at (row / 8) * 256 + (t / 4) * 32 + (row % 8) * 4 + t % 4 floats.
+template <int NC>
 __global__ void __launch_bounds__(kThreads, 1)
-    reduce4_tc05_kernel(const float4* __restrict__ in, int B, int n_red, float* __restrict__ out) {
+    reduce_tc05_kernel(const float* __restrict__ in_f, int B, int n_red, float* __restrict__ out) {
+  constexpr int kRpt = NC == 4 ? kRedPerTile : kRedPerTile / 2;  // reductions per 128-row tile
   extern __shared__ __align__(1024) unsigned char raw[];
   Smem& sm = *reinterpret_cast<Smem*>(raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const float4* in = reinterpret_cast<const float4*>(in_f);
 
   if (warp == 0) {  // TMEM: 32 columns (D uses 16)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(smem_u32(&sm.tmem_base)));
@@ -145,6 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
   for (int i = tid; i < kN * 8; i += kThreads) sm.ones[i] = 1.0f;
+  if (NC == 7)  // the padding rows (component 7) are never written: zero them once
+    for (int i = tid; i < 2 * kRedPerTile * kChunk * 4; i += kThreads) {
+      (&sm.hi[0][0])[i] = 0.f;
+      (&sm.lo[0][0])[i] = 0.f;
+    }
   asm volatile("fence.proxy.async.shared::cta;\n");
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -157,50 +185,73 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   uint32_t phase[2] = {0u, 0u};
   int uses[2] = {0, 0};
-  float4 xr[8];
+  float4 xr[NC == 4 ? 8 : 1];
+  float xs[NC == 7 ? 28 : 1];
   bool have = false;
-  const int n_tiles = (n_red + kRedPerTile - 1) / kRedPerTile;
+  const int n_tiles = (n_red + kRpt - 1) / kRpt;
   const int chunks = B / kChunk;
+  auto load = [&](int r0, int ch) {
+    if constexpr (NC == 4)
+      load_chunk(in, B, n_red, r0, ch, warp, lane, xr);
+    else
+      load_chunk7(in_f, B, n_red, r0, ch, warp, lane, xs);
+  };
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int r0 = tile * kRedPerTile;
+    const int r0 = tile * kRpt;
     for (int ch = 0; ch < chunks; ++ch) {
       const int s = ch & 1;
       if (uses[s] > 0) {  // previous MMAs reading stage s must be done
         mbar_wait(&sm.mbar[s], phase[s]);
         phase[s] ^= 1u;
       }
-      // 32 reductions x 32 records = 1024 float4 per chunk, 8 per thread.
-      // Lane l holds record t = 16*half + (l & 15) of reduction
-      // r = 2*pair + (l >> 4): two coalesced 256-byte runs per warp.  The
-      // K-major core-matrix position of component c is
-      //   pair*1024 + (t/4)*128 + (4*(l>>4) + c)*16 + (t%4)*4  bytes,
-      // and storing component (c0 + s) % 4 at step s (c0 = (l>>2)&3) makes
-      // the 32 lanes hit 32 distinct banks.
-      const int c0 = (lane >> 2) & 3;
-      if (!have) load_chunk(in, B, n_red, r0, ch, warp, lane, xr);
+      if (!have) load(r0, ch);
       have = false;
+      if constexpr (NC == 4) {
+        // 32 reductions x 32 records = 1024 float4 per chunk, 8 per thread.
+        // Lane l holds record t = 16*half + (l & 15) of reduction
+        // r = 2*pair + (l >> 4): two coalesced 256-byte runs per warp.  The
+        // K-major core-matrix position of component c is
+        //   pair*1024 + (t/4)*128 + (4*(l>>4) + c)*16 + (t%4)*4  bytes,
+        // and storing component (c0 + s) % 4 at step s (c0 = (l>>2)&3) makes
+        // the 32 lanes hit 32 distinct banks.
+        const int c0 = (lane >> 2) & 3;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int combo = warp * 8 + q, pair = combo >> 1, half = combo & 1;
-        const int t = 16 * half + (lane & 15);
-        const float4 x = xr[q];
-        const int base = pair * 256 + (t >> 2) * 32 + 4 * (lane >> 4) * 4 + (t & 3);  // in floats
+        for (int q = 0; q < 8; ++q) {
+          const int combo = warp * 8 + q, pair = combo >> 1, half = combo & 1;
+          const int t = 16 * half + (lane & 15);
+          const float4 x = xr[q];
+          const int base = pair * 256 + (t >> 2) * 32 + 4 * (lane >> 4) * 4 + (t & 3);  // in floats
 #pragma unroll
-        for (int st = 0; st < 4; ++st) {
-          const int c = (c0 + st) & 3;
-          const float v = sel4(x, c);
-          const float h = __uint_as_float(trunc_tf32(v));
-          sm.hi[s][base + c * 4] = h;
-          sm.lo[s][base + c * 4] = v - h;
+          for (int st = 0; st < 4; ++st) {
+            const int c = (c0 + st) & 3;
+            const float v = sel4(x, c);
+            const float h = __uint_as_float(trunc_tf32(v));
+            sm.hi[s][base + c * 4] = h;
+            sm.lo[s][base + c * 4] = v - h;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 4 * warp + j;
+#pragma unroll
+          for (int q = 0; q < 7; ++q) {
+            const int f = lane + 32 * q, t = f / 7, c = f - 7 * t;
+            const int at = r * 256 + (t >> 2) * 32 + c * 4 + (t & 3);
+            const float v = xs[7 * j + q];
+            const float h = __uint_as_float(trunc_tf32(v));
+            sm.hi[s][at] = h;
+            sm.lo[s][at] = v - h;
+          }
         }
       }
       // prefetch the next chunk (this tile's or the next tile's first) so
       // its HBM latency overlaps the barrier and the MMA issue
       if (ch + 1 < chunks) {
-        load_chunk(in, B, n_red, r0, ch + 1, warp, lane, xr);
+        load(r0, ch + 1);
         have = true;
       } else if (tile + (int)gridDim.x < n_tiles) {
-        load_chunk(in, B, n_red, r0 + (int)gridDim.x * kRedPerTile, 0, warp, lane, xr);
+        load(r0 + (int)gridDim.x * kRpt, 0);
         have = true;
       }
       asm volatile("fence.proxy.async.shared::cta;\n");
@@ -211,8 +262,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < kChunk / 8; ++k) {
           // A: K-major, core matrix = 8 rows x 4 records (128 B); next
-          // 4-record group +128 B (LBO), next 8 rows (2 reductions) +1024 B
-          // (SBO); one MMA (K = 8) spans two groups -> +256 B per k-step
+          // 4-record group +128 B (LBO), next 8 rows +1024 B (SBO); one MMA
+          // (K = 8) spans two groups -> +256 B per k-step
           const uint64_t dh = make_desc(ah + k * 256, 128, 1024);
           const uint64_t dl = make_desc(al + k * 256, 128, 1024);
           mma_tf32(tmem, dh, bdesc, idesc, (ch > 0 || k > 0) ? 1u : 0u);
@@ -238,8 +289,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-    const int row = warp * 32 + lane;  // = 4 * reduction + component
-    if (r0 + (row >> 2) < n_red) out[(size_t)r0 * 4 + row] = __uint_as_float(v);
+    const int row = warp * 32 + lane;
+    if constexpr (NC == 4) {  // row = 4 * reduction + component
+      if (r0 + (row >> 2) < n_red) out[(size_t)r0 * 4 + row] = __uint_as_float(v);
+    } else {  // row = 8 * reduction + component
+      const int r = row >> 3, c = row & 7;
+      if (c < 7 && r0 + r < n_red) out[(size_t)(r0 + r) * 7 + c] = __uint_as_float(v);
+    }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();  // D is overwritten by the next tile's first MMA
   }
@@ -425,16 +481,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
 }  // namespace tc05
 
-cudaError_t launch_reduce4_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s) {
+template <int NC>
+static cudaError_t launch_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s) {
+  if (n_red <= 0) return cudaSuccess;
   const size_t smem = sizeof(tc05::Smem) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(tc05::reduce4_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(tc05::reduce_tc05_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  const int tiles = (n_red + tc05::kRedPerTile - 1) / tc05::kRedPerTile;
+  const int rpt = NC == 4 ? tc05::kRedPerTile : tc05::kRedPerTile / 2;
+  const int tiles = (n_red + rpt - 1) / rpt;
   int grid = 148 * ctas_per_sm;
   if (grid > tiles) grid = tiles;
-  tc05::reduce4_tc05_kernel<<<grid, tc05::kThreads, smem, s>>>(reinterpret_cast<const float4*>(in), B, n_red, out);
+  tc05::reduce_tc05_kernel<NC><<<grid, tc05::kThreads, smem, s>>>(in, B, n_red, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_reduce4_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s) {
+  return launch_tc05<4>(in, B, n_red, out, ctas_per_sm, s);
+}
+cudaError_t launch_reduce7_tc05(const float* in, int B, int n_red, float* out, int ctas_per_sm, cudaStream_t s) {
+  return launch_tc05<7>(in, B, n_red, out, ctas_per_sm, s);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)

@@ -315,25 +315,42 @@ def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch
     lane.close()
 
 
-def test_warp_pair_search_bit_identical(instances, monkeypatch):
-    """FP64-fast chunked ligands run each Lamarckian search on a warp pair
-    (lga_ls_pair_kernel: the helper warp takes half of every evaluation's
-    chunk items).  Same items, same arithmetic, same combine order as the
-    one-warp kernel (MDR_LS_PAIR=0), so whole LGA runs are bit-identical."""
+@pytest.mark.parametrize("warps", [0, 2, 3, 4])
+def test_multi_warp_search_bit_identical(instances, monkeypatch, warps):
+    """FP64-fast chunked ligands run each Lamarckian search of the LGA on
+    several warps (ls_multi.cu, `warps` per search; 0 = the legacy warp-pair
+    kernel): the helpers take chunk items of every evaluation, the leader
+    keeps the genotype in registers.  Same items, same arithmetic, same
+    combine order as the one-warp kernel, so with the same site chunking
+    (pinned here: MDR_CHUNK_LEN = MDR_LS_CHUNK_LEN = 8) whole LGA runs are
+    bit-identical.  Covers a 40-torsion ligand (dim 46 > 32: the multi-warp
+    kernel falls back to the legacy pair kernel)."""
     from paper_2410_10447_b200.workloads import c3
 
-    pair = Device(0, pair=PAIR_FP64_FAST)
-    monkeypatch.setenv("MDR_LS_PAIR", "0")
+    monkeypatch.setenv("MDR_CHUNK_LEN", "8")
+    monkeypatch.setenv("MDR_LS_CHUNK_LEN", "8")
+    multi = Device(0, pair=PAIR_FP64_FAST)
+    assert multi.lib.mdr_ctx_set_ls_warps(multi.ctx, warps) == 0
     single = Device(0, pair=PAIR_FP64_FAST)
+    assert single.lib.mdr_ctx_set_ls_warps(single.ctx, 1) == 0
     rng = derive_rng(93, "pair/identity")
     cases = [c3(), random_instance(rng, 3, 28, 64), random_instance(rng, 40, 16, 64)]
     seeds = np.arange(16, dtype=np.uint64) + np.uint64(4321)
     for inst in cases:
-        for method in (BASELINE, TCU_SPLIT):
-            a = pair.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
+        for method in (BASELINE, TCU_SPLIT, TCU):
+            a = multi.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
             b = single.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
             for x, y in zip(a, b):
                 assert x.best_energy == y.best_energy and x.evaluations == y.evaluations
                 assert np.array_equal(x.best_genotype, y.best_genotype)
-    pair.close()
+    multi.close()
     single.close()
+
+
+def test_branch_free_sqrt_is_ieee(dev):
+    """The multi-warp search's dsqrt_rn must equal IEEE sqrt bit for bit."""
+    import ctypes as C
+
+    bad = C.c_uint64()
+    assert dev.lib.mdr_selftest_dsqrt(dev.ctx, 12345, 200_000_000, C.byref(bad)) == 0
+    assert bad.value == 0

@@ -181,3 +181,49 @@ def test_branch_free_division_is_ieee(dev):
     bad = C.c_uint64()
     rc = dev.lib.mdr_selftest_ddiv(dev.ctx, 2024, 200_000_000, C.byref(bad))
     assert rc == 0 and bad.value == 0, bad.value
+
+
+# ---- TcuSplit batches routed to the tcgen05 contraction (tc05_reduce.cu)
+@pytest.mark.parametrize("n", [32, 64, 128, 256])
+def test_reduce4_split_tcgen05_route(dev, n):
+    """A TcuSplit batch of >= 148*32 reductions of a multiple of 32 records
+    runs as one batched tcgen05 contraction (reduce.cpp:80-111 semantics,
+    fp32-accurate: |err| <= 1e-6 * sum|x| against float64), with a ragged
+    last tile; the warp-per-reduction mma.sync kernel (route off) obeys the
+    same bound."""
+    n_red = 148 * 32 + 37
+    assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, n, n_red) == 1
+    assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, n + 16, n_red) == 0
+    assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, n, 100) == 0
+    assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, BASELINE, n, n_red) == 0
+    rng = np.random.default_rng(n)
+    v = (rng.uniform(-1, 1, (n_red, n, 4)) * 10.0 ** rng.integers(-6, 4, (n_red, 1, 4))).astype(np.float32)
+    exact = v.astype(np.float64).sum(1)
+    mass = np.abs(v.astype(np.float64)).sum(1)
+    got, st = dev.reduce4_batch(v, SINGLE, TCU_SPLIT)
+    assert np.all(np.abs(got - exact) <= 1e-6 * mass + 1e-30)
+    dev.lib.mdr_ctx_set_tc05(dev.ctx, 0)
+    try:
+        warp, st2 = dev.reduce4_batch(v, SINGLE, TCU_SPLIT)
+    finally:
+        dev.lib.mdr_ctx_set_tc05(dev.ctx, 1)
+    assert np.all(np.abs(warp - exact) <= 1e-6 * mass + 1e-30)
+    assert st == st2  # the reference-model counters do not depend on the route
+
+
+@pytest.mark.parametrize("n", [32, 64, 128])
+def test_reduce7_split_tcgen05_route(dev, n):
+    """Partial7 records (reduce7 reduce.cpp:165-209) through the tcgen05
+    contraction: 16 reductions x 8 rows per tile, ragged tail."""
+    n_red = 148 * 32 + 21
+    assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, n, n_red) == 1
+    rng = np.random.default_rng(100 + n)
+    r = (rng.uniform(-1, 1, (n_red, n, 7)) * 10.0 ** rng.integers(-5, 3, (n_red, 1, 7))).astype(np.float32)
+    got, _ = dev.reduce7_batch(r, TCU_SPLIT, SINGLE)
+    exact = r.astype(np.float64).sum(1)
+    mass = np.abs(r.astype(np.float64)).sum(1)
+    assert np.all(np.abs(got - exact) <= 1e-6 * mass + 1e-30)
+    # integer records: exact
+    ri = rng.integers(0, 2, (n_red, n, 7)).astype(np.float32)
+    got, _ = dev.reduce7_batch(ri, TCU_SPLIT, SINGLE)
+    assert np.array_equal(got, ri.sum(1))
