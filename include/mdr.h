@@ -132,13 +132,17 @@ int mdr_ctx_set_exact_torsion(mdr_ctx* ctx, int on);
  * LGA init / offspring, one-warp search, polish); *n_chunks = 1 means lane
  * per atom (always the case for the other pair modes).  DESIGN.md §3. */
 int mdr_site_chunking(int pair_precision, int n_atoms, int n_sites, int* n_chunks, int* chunk_len);
-/* The same policy for the LGA's Lamarckian search on `warps` warps per
- * search (its items spread over 32 * warps lanes; the default context runs
- * 2, mdr_ctx_set_ls_warps). */
-int mdr_search_chunking(int pair_precision, int n_atoms, int n_sites, int warps, int* n_chunks, int* chunk_len);
-/* Warps per Lamarckian search of the LGA (default 2; 1 = one warp per
- * search, 0 = the legacy warp-pair kernel; env MDR_LS_WARPS).  Every choice
- * gives bit-identical results for the same chunking. */
+/* The same policy for the LGA's Lamarckian search on `warps` (1 or 2) warps
+ * per search (the default context runs 2, mdr_ctx_set_ls_warps).  On two
+ * warps an item is (chunk, group of *atoms_per_item atoms): 1, or 3 when
+ * register blocking shortens nothing on the critical path but cuts the
+ * shared-memory site loads (C3: 8 chunks of 8 sites, 3 atoms per item). */
+int mdr_search_chunking(int pair_precision, int n_atoms, int n_sites, int warps, int* n_chunks, int* chunk_len,
+                        int* atoms_per_item);
+/* Warps per Lamarckian search of the LGA (default 2 = the leader/helper
+ * search of ls_multi.cu; 1 = one warp per search, 0 = the legacy warp-pair
+ * kernel; env MDR_LS_WARPS).  Every choice gives bit-identical results for
+ * the same chunking.  Set before the first docking of the context. */
 int mdr_ctx_set_ls_warps(mdr_ctx* ctx, int warps);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);
@@ -198,6 +202,9 @@ int mdr_ctx_set_tc05(mdr_ctx* ctx, int on);
 /* Self test: bit mismatches of the branch-free FP64 square root of the LGA
  * search against IEEE sqrt.rn.f64 over n counter-generated arguments. */
 int mdr_selftest_dsqrt(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
+/* Self test: bit mismatches (sin and cos counted separately) of the
+ * branch-free sincos of the LGA search against libdevice sincos. */
+int mdr_selftest_sincos(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
 int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches);
 /* Self test: the device's correctly rounded sin, cos (angles in [-pi, pi)),
  * log (Box-Muller u1) and cos(2 pi u2) (crmath.cuh), then CUDA libdevice's,

@@ -34,7 +34,7 @@ _SIGS = {
     "mdr_ctx_set_cta_warps": (I, [P, I]),
     "mdr_ctx_set_exact_torsion": (I, [P, I]),
     "mdr_site_chunking": (I, [I, I, I, P, P]),
-    "mdr_search_chunking": (I, [I, I, I, I, P, P]),
+    "mdr_search_chunking": (I, [I, I, I, I, P, P, P]),
     "mdr_ctx_set_ls_warps": (I, [P, I]),
     "mdr_last_error": (C.c_char_p, [P]),
     "mdr_ctx_launch_count": (U64, [P]),
@@ -69,6 +69,7 @@ _SIGS = {
     "mdr_lga_batch_profile_dev": (I, [P, P, P, P, P, P]),
     "mdr_selftest_ddiv": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_dsqrt": (I, [P, U64, C.c_int64, P]),
+    "mdr_selftest_sincos": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_crmath": (I, [P, C.c_int64, P]),
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_reduce_bench_kernels": (I, []),

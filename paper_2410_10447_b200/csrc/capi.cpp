@@ -56,8 +56,10 @@ struct mdr_ctx {
   int chunk_len = 0;  // > 0: pin the chunk length (MDR_CHUNK_LEN, timing only)
   int ls_pair = 1;    // warp-pair Lamarckian searches (MDR_LS_PAIR=0 disables)
   int tc05 = 1;       // TcuSplit batched reductions on tcgen05 where they win (MDR_TC05=0 disables)
-  int ls_warps = 2;   // warps per LGA Lamarckian search (ls_multi.cu; MDR_LS_WARPS, 0 = legacy pair kernel)
+  int ls_warps = 2;   // warps per LGA Lamarckian search: 2 = ls_multi.cu, 1 = one warp, 0 = legacy pair kernel (MDR_LS_WARPS)
   int ls_chunk_len = 0;  // > 0: pin the search's chunk length (MDR_LS_CHUNK_LEN, timing only)
+  int ls_stagger = 0;    // start offset of odd searches in cycles (MDR_LS_STAGGER)
+  int ls_group = 0;      // > 0: pin the search's atoms per item (MDR_LS_GROUP: 1 or 3)
 
   std::string err;
   uint64_t launches = 0;
@@ -229,6 +231,38 @@ void pick_chunks(int na, int ns, int search_lanes, int force_len, int& n_chunks,
   }
 }
 
+// Items of the two-warp LGA search (ls_multi.cu): (chunk of len sites,
+// group of G atoms) over 64 lanes; the critical path is rounds x G x len
+// pair terms per lane, G = 1 preferred on ties.  C3 (20 atoms x 64 sites):
+// G = 1, len 8 -> 160 items, 3 rounds x 8; G = 3, len 8 -> 56 items, 1
+// round x 24: equal path and a third of the site loads, but measured
+// 200.3 vs 179.9 M evals/s (G = 3 holds 6 pair terms in flight per lane at
+// 128 registers, G = 1 eight; profiles/r2_ls_multi_ab.json).
+void pick_search_items(int na, int ns, int force_len, int force_group, int& n_chunks, int& chunk_len, int& group) {
+  constexpr int kBatch = 8;
+  n_chunks = 1;
+  chunk_len = ns;
+  group = 1;
+  long best = (long)((na + 31) / 32) * ns;
+  for (int G : {1, 3}) {
+    if (force_group > 0 && G != force_group) continue;
+    for (int len = kBatch; len < ns; len += kBatch) {
+      const int n = (ns + len - 1) / len;
+      if (na * n > kMaxChunkItems || na * n <= 32) continue;
+      const int items = (na + G - 1) / G * n;
+      const long cost = (long)((items + 63) / 64) * G * len;
+      if (force_len > 0 ? len == force_len : cost < best) {
+        best = cost;
+        n_chunks = n;
+        chunk_len = len;
+        group = G;
+        if (force_len > 0) break;
+      }
+    }
+    if (force_len > 0 && n_chunks > 1) break;
+  }
+}
+
 LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   LigandView L = di->view;
   L.exact_torsion = c->exact;
@@ -236,17 +270,22 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   L.chunk_len = L.n_sites;
   L.ls_pair = c->ls_pair;
   L.ls_warps = c->ls_warps;
+  L.ls_stagger = c->ls_stagger;
   L.ls_n_chunks = 1;
   L.ls_chunk_len = L.n_sites;
   // the warp-per-pose kernels (score, init, offspring, one-warp search,
   // polish) spread chunk items over 32 lanes; the LGA's multi-warp search
-  // over its own 32 * ls_warps (the legacy pair kernel: 64)
-  const bool multi = c->ls_pair && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
-  const int search_lanes = !multi ? 32 : (c->ls_warps >= 2 ? 32 * c->ls_warps : 64);
+  // over the 64 lanes of its warp pair (ls_multi.cu or the legacy kernel)
+  const bool multi = c->ls_pair && c->ls_warps != 1 && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
+  const int search_lanes = multi ? 64 : 32;
+  L.ls_group = 1;
   if (c->pair == MDR_PAIR_FP64_FAST && c->chunking) {
     pick_chunks(L.n_atoms, L.n_sites, 32, c->chunk_len, L.n_chunks, L.chunk_len);
-    pick_chunks(L.n_atoms, L.n_sites, search_lanes, c->ls_chunk_len > 0 ? c->ls_chunk_len : c->chunk_len,
-                L.ls_n_chunks, L.ls_chunk_len);
+    const int force = c->ls_chunk_len > 0 ? c->ls_chunk_len : c->chunk_len;
+    if (multi && c->ls_warps == 2)
+      pick_search_items(L.n_atoms, L.n_sites, force, c->ls_group, L.ls_n_chunks, L.ls_chunk_len, L.ls_group);
+    else
+      pick_chunks(L.n_atoms, L.n_sites, search_lanes, force, L.ls_n_chunks, L.ls_chunk_len);
   }
   return L;
 }
@@ -288,6 +327,8 @@ mdr_ctx* mdr_ctx_create(int device) {
   if (const char* v = std::getenv("MDR_TC05")) c->tc05 = std::atoi(v) != 0;
   if (const char* v = std::getenv("MDR_LS_WARPS")) c->ls_warps = std::atoi(v);
   if (const char* v = std::getenv("MDR_LS_CHUNK_LEN")) c->ls_chunk_len = std::atoi(v);
+  if (const char* v = std::getenv("MDR_LS_STAGGER")) c->ls_stagger = std::atoi(v);
+  if (const char* v = std::getenv("MDR_LS_GROUP")) c->ls_group = std::atoi(v);
   return c;
 }
 
@@ -320,19 +361,26 @@ int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
 }
 
 int mdr_ctx_set_ls_warps(mdr_ctx* c, int w) {
-  if (!c || w < 0 || w > 4) return fail(c, MDR_ERR_INVALID, "search warps must be 0..4 (0 = legacy warp pair)");
+  if (!c || w < 0 || w > 2) return fail(c, MDR_ERR_INVALID, "search warps must be 0..2 (0 = legacy warp pair)");
   c->ls_warps = w;
   c->ls_pair = w != 1;
   return MDR_OK;
 }
 
-int mdr_search_chunking(int pair, int na, int ns, int warps, int* n_chunks, int* chunk_len) {
-  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || warps < 1 || warps > 4 || pair < MDR_PAIR_FP64 ||
+int mdr_search_chunking(int pair, int na, int ns, int warps, int* n_chunks, int* chunk_len, int* atoms_per_item) {
+  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || warps < 1 || warps > 2 || pair < MDR_PAIR_FP64 ||
       pair > MDR_PAIR_FP64_FAST)
     return fail(nullptr, MDR_ERR_INVALID, "bad argument");
   *n_chunks = 1;
   *chunk_len = ns;
-  if (pair == MDR_PAIR_FP64_FAST) pick_chunks(na, ns, 32 * warps, 0, *n_chunks, *chunk_len);
+  int group = 1;
+  if (pair == MDR_PAIR_FP64_FAST) {
+    if (warps == 2)
+      pick_search_items(na, ns, 0, 0, *n_chunks, *chunk_len, group);
+    else
+      pick_chunks(na, ns, 32, 0, *n_chunks, *chunk_len);
+  }
+  if (atoms_per_item) *atoms_per_item = group;
   return MDR_OK;
 }
 
@@ -568,6 +616,21 @@ int mdr_ctx_set_tc05(mdr_ctx* ctx, int on) {
 
 int mdr_reduce_uses_tc05(mdr_ctx* ctx, int method, int n, int n_red) {
   return ctx && use_tc05(ctx, method, n, n_red) ? 1 : 0;
+}
+
+// Self test of the branch-free libdevice sincos (mdr_device.cuh sincos_fast).
+int mdr_selftest_sincos(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatches) {
+  if (!ctx || !mismatches || n < 0) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  DevBuf<unsigned long long> d;
+  CK(d.alloc(1, S(ctx)));
+  CK(cudaMemsetAsync(d.p, 0, sizeof(unsigned long long), S(ctx)));
+  CK(launch_sincos_selftest(seed, (long long)n, d.p, S(ctx)));
+  ctx->launches++;
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d.p, sizeof h, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  *mismatches = h;
+  return MDR_OK;
 }
 
 // Self test of the branch-free FP64 square root of the LGA search (ls_multi.cu).

@@ -1148,7 +1148,7 @@ bool phase_prof_read(unsigned long long* out16, bool reset) {
     unsigned long long z[16] = {};
     if (cudaMemcpyToSymbol(g_phase, z, sizeof(z)) != cudaSuccess) return false;
   }
-  return true;
+  return phase_prof_read_multi(out16, reset);  // ls_multi.cu's counters (one search kernel runs at a time)
 #else
   (void)out16;
   (void)reset;

@@ -61,7 +61,9 @@ cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int 
 
 cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s);
 bool phase_prof_read(unsigned long long* out16, bool reset);
+bool phase_prof_read_multi(unsigned long long* out16, bool reset);  // adds ls_multi.cu's counters
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
+cudaError_t launch_sincos_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_dsqrt_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 
 // ls_multi.cu: the LGA's Lamarckian search on L.ls_warps warps per search

@@ -45,27 +45,31 @@ def test_site_chunking_policy():
         assert lib.mdr_site_chunking(pair, na, ns, ctypes.byref(n), ctypes.byref(ln)) == 0
         return n.value, ln.value
 
-    def pick_search(pair, na, ns, warps):
-        n, ln = ctypes.c_int(), ctypes.c_int()
-        assert lib.mdr_search_chunking(pair, na, ns, warps, ctypes.byref(n), ctypes.byref(ln)) == 0
-        return n.value, ln.value
+    def pick_search(pair, na, ns, warps, group=False):
+        n, ln, g = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        assert lib.mdr_search_chunking(pair, na, ns, warps, ctypes.byref(n), ctypes.byref(ln), ctypes.byref(g)) == 0
+        return (n.value, ln.value, g.value) if group else (n.value, ln.value)
 
     assert pick(PAIR_FP64_FAST, 20, 64) == (3, 24)  # C3 on one warp: 60 items in 2 rounds of 24 sites
-    assert pick_search(PAIR_FP64_FAST, 20, 64, 2) == (8, 8)  # C3's search on 2 warps: measured best
+    # C3's search on 2 warps: 8 chunks of 8 sites, one atom per item (160 items, 3 rounds of 64 lanes)
+    assert pick_search(PAIR_FP64_FAST, 20, 64, 2, group=True) == (8, 8, 1)
     assert pick_search(PAIR_FP64_FAST, 20, 64, 1) == pick(PAIR_FP64_FAST, 20, 64)
     assert pick(PAIR_FP64, 20, 64) == (1, 64)
     assert pick(PAIR_FP32, 20, 64) == (1, 64)
     assert pick_search(PAIR_FP32, 20, 64, 2) == (1, 64)
     assert pick(PAIR_FP64_FAST, 200, 64) == (1, 64)  # items would exceed 256
     assert pick(PAIR_FP64_FAST, 20, 6) == (1, 6)  # fewer sites than one batch
-    for warps in (1, 2, 3, 4):
+    for warps in (1, 2):
         for na in (1, 5, 16, 31, 40, 100, 128):
             for ns in (8, 30, 64, 200):
-                n, ln = pick_search(PAIR_FP64_FAST, na, ns, warps)
+                n, ln, g = pick_search(PAIR_FP64_FAST, na, ns, warps, group=True)
                 if n > 1:
                     assert ln % 8 == 0 and na * n <= 256 and (n - 1) * ln < ns <= n * ln
-                    lanes = 32 * warps if warps > 1 and na * n > 32 else 32
-                    assert ((na * n + lanes - 1) // lanes) * (ln + (0 if lanes > 32 else 4)) < ((na + 31) // 32) * ns
-    assert lib.mdr_search_chunking(PAIR_FP64_FAST, 20, 64, 5, ctypes.byref(ctypes.c_int()),
-                                   ctypes.byref(ctypes.c_int())) != 0
+                    if warps == 1:
+                        assert g == 1 and ((na * n + 31) // 32) * (ln + 4) < ((na + 31) // 32) * ns
+                    else:
+                        assert g in (1, 3) and na * n > 32
+                        assert ((-(-na // g) * n + 63) // 64) * g * ln < ((na + 31) // 32) * ns
+    assert lib.mdr_search_chunking(PAIR_FP64_FAST, 20, 64, 3, ctypes.byref(ctypes.c_int()),
+                                   ctypes.byref(ctypes.c_int()), None) != 0
     assert lib.mdr_site_chunking(7, 20, 64, ctypes.byref(ctypes.c_int()), ctypes.byref(ctypes.c_int())) != 0

@@ -315,12 +315,13 @@ def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch
     lane.close()
 
 
-@pytest.mark.parametrize("warps", [0, 2, 3, 4])
-def test_multi_warp_search_bit_identical(instances, monkeypatch, warps):
+@pytest.mark.parametrize("warps,group", [(0, 0), (2, 1), (2, 3)])
+def test_multi_warp_search_bit_identical(instances, monkeypatch, warps, group):
     """FP64-fast chunked ligands run each Lamarckian search of the LGA on
-    several warps (ls_multi.cu, `warps` per search; 0 = the legacy warp-pair
-    kernel): the helpers take chunk items of every evaluation, the leader
-    keeps the genotype in registers.  Same items, same arithmetic, same
+    two warps (ls_multi.cu, warps = 2; 0 = the legacy warp-pair kernel): the
+    helper takes chunk items of every evaluation, the leader keeps the
+    genotype in registers; an item is one chunk of sites against 1 or 3
+    atoms.  Same items, same arithmetic, same
     combine order as the one-warp kernel, so with the same site chunking
     (pinned here: MDR_CHUNK_LEN = MDR_LS_CHUNK_LEN = 8) whole LGA runs are
     bit-identical.  Covers a 40-torsion ligand (dim 46 > 32: the multi-warp
@@ -329,6 +330,8 @@ def test_multi_warp_search_bit_identical(instances, monkeypatch, warps):
 
     monkeypatch.setenv("MDR_CHUNK_LEN", "8")
     monkeypatch.setenv("MDR_LS_CHUNK_LEN", "8")
+    if group:
+        monkeypatch.setenv("MDR_LS_GROUP", str(group))  # atoms per chunk item (register blocking)
     multi = Device(0, pair=PAIR_FP64_FAST)
     assert multi.lib.mdr_ctx_set_ls_warps(multi.ctx, warps) == 0
     single = Device(0, pair=PAIR_FP64_FAST)
@@ -353,4 +356,14 @@ def test_branch_free_sqrt_is_ieee(dev):
 
     bad = C.c_uint64()
     assert dev.lib.mdr_selftest_dsqrt(dev.ctx, 12345, 200_000_000, C.byref(bad)) == 0
+    assert bad.value == 0
+
+
+def test_branch_free_sincos_is_libdevice(dev):
+    """The multi-warp search's sincos_fast must equal libdevice sincos bit
+    for bit (angles in [-pi, pi) and magnitudes 2^-30 .. 2^30)."""
+    import ctypes as C
+
+    bad = C.c_uint64()
+    assert dev.lib.mdr_selftest_sincos(dev.ctx, 777, 200_000_000, C.byref(bad)) == 0
     assert bad.value == 0

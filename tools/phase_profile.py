@@ -18,6 +18,8 @@ sys.path.insert(0, ROOT)
 
 NAMES = ["L0 adadelta", "L1 trig+frame+pos", "L2 wait B1", "L3 items", "L4 wait B2", "L5 combine+reduce",
          "L6 project+best", None, "H8 wait B1", "H9 items", "H10 wait B2"]
+# ls_multi.cu (default search kernel): L1 = trig, frame, positions and the
+# B1 arrive (no wait), L2 unused, H10 = the projection axes (last helper)
 
 
 def main():

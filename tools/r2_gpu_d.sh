@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_dock.py -x -q -p no:cacheprovider -k "multi_warp or sqrt or sincos" > gpurun_out/r2d_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r2d_tests.txt
+tail -5 gpurun_out/r2d_tests.txt
+MDR_LIB_PATH=paper_2410_10447_b200/variants/prof/libmdr_b200.so PHASE_OUT=r2d_phase.json timeout 300 python tools/phase_profile.py > gpurun_out/r2d_phase.txt 2>&1; cat gpurun_out/r2d_phase.txt
+AB_OUT=r2d_ab.json timeout 900 python tools/ls_ab.py "MDR_LS_WARPS=0" "MDR_LS_WARPS=2" "MDR_LS_WARPS=2 MDR_LS_CHUNK_LEN=16"
