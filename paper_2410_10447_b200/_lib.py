@@ -25,6 +25,7 @@ SZ = C.c_size_t
 _SIGS = {
     "mdr_version": (C.c_char_p, []),
     "mdr_phase_prof": (I, [P, I]),
+    "mdr_phase_prof_sm": (I, [P, I]),
     "mdr_ctx_create": (P, [I]),
     "mdr_ctx_destroy": (None, [P]),
     "mdr_ctx_set_stream": (I, [P, P]),

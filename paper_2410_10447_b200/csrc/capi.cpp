@@ -58,7 +58,6 @@ struct mdr_ctx {
   int tc05 = 1;       // TcuSplit batched reductions on tcgen05 where they win (MDR_TC05=0 disables)
   int ls_warps = 2;   // warps per LGA Lamarckian search: 2 = ls_multi.cu, 1 = one warp, 0 = legacy pair kernel (MDR_LS_WARPS)
   int ls_chunk_len = 0;  // > 0: pin the search's chunk length (MDR_LS_CHUNK_LEN, timing only)
-  int ls_stagger = 0;    // start offset of odd searches in cycles (MDR_LS_STAGGER)
   int ls_group = 0;      // > 0: pin the search's atoms per item (MDR_LS_GROUP: 1 or 3)
 
   std::string err;
@@ -270,7 +269,6 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   L.chunk_len = L.n_sites;
   L.ls_pair = c->ls_pair;
   L.ls_warps = c->ls_warps;
-  L.ls_stagger = c->ls_stagger;
   L.ls_n_chunks = 1;
   L.ls_chunk_len = L.n_sites;
   // the warp-per-pose kernels (score, init, offspring, one-warp search,
@@ -312,6 +310,15 @@ int mdr_phase_prof(uint64_t* out16, int reset) {
   return MDR_OK;
 }
 
+int mdr_phase_prof_sm(uint32_t* out256, int reset) {
+  if (!out256) return fail(nullptr, MDR_ERR_INVALID, "null argument");
+  unsigned v[256];
+  if (!sm_searches_read(v, reset != 0))
+    return fail(nullptr, MDR_ERR_INVALID, "not a phase-profiling build (-DMDR_PHASE_PROF=1)");
+  for (int k = 0; k < 256; ++k) out256[k] = v[k];
+  return MDR_OK;
+}
+
 mdr_ctx* mdr_ctx_create(int device) {
   if (cudaSetDevice(device) != cudaSuccess) return nullptr;
   mdr_ctx* c = new mdr_ctx;
@@ -327,7 +334,6 @@ mdr_ctx* mdr_ctx_create(int device) {
   if (const char* v = std::getenv("MDR_TC05")) c->tc05 = std::atoi(v) != 0;
   if (const char* v = std::getenv("MDR_LS_WARPS")) c->ls_warps = std::atoi(v);
   if (const char* v = std::getenv("MDR_LS_CHUNK_LEN")) c->ls_chunk_len = std::atoi(v);
-  if (const char* v = std::getenv("MDR_LS_STAGGER")) c->ls_stagger = std::atoi(v);
   if (const char* v = std::getenv("MDR_LS_GROUP")) c->ls_group = std::atoi(v);
   return c;
 }
@@ -1175,6 +1181,7 @@ static mdr_lga_batch* lga_batch_alloc(mdr_ctx* ctx, int method, int accum, const
   parts.push_back({(void**)&D.recs, sizeof(mdr_ls_record) * Rr * D.maxrec});
   parts.push_back({(void**)&D.conv, sizeof(int) * Rr});
   parts.push_back({(void**)&D.status, sizeof(int) * Rr});
+  parts.push_back({(void**)&D.ls_next, sizeof(int) * (size_t)std::max(D.gens, 1)});
   parts.push_back({(void**)&b->seeds, sizeof(uint64_t) * Rr});
   for (auto& p : parts) off += al(p.second);
   if (cudaMalloc(&b->block, off) != cudaSuccess || cudaMemset(b->block, 0, off) != cudaSuccess) {

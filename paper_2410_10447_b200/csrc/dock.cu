@@ -673,6 +673,8 @@ __global__ void lga_init_finalize(LgaDev D) {
     D.status[run] = MDR_OK;
     D.active[run] = D.gens > 0 && budget_ok(D, D.P);
   }
+  if (run == 0)  // work counters of the persistent search kernel, one per generation
+    for (int g = lane; g < D.gens; g += 32) D.ls_next[g] = 0;
 }
 
 // Bookkeeping of one generation, warp per run, with the reference's
@@ -1042,7 +1044,7 @@ cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int 
   if (cta_warps > 0) {
     if (e == cudaSuccess) e = prep_lga_ls_cta_kernel(method, pair, cta_smem(L, cta_warps));
   } else if (ls_multi_supported(L, pair, wpb, cta_warps)) {
-    if (e == cudaSuccess) e = prep_ls_multi(L, method, smem);
+    if (e == cudaSuccess) e = prep_ls_multi(L, method);
   } else if (use_ls_pair(L, pair, wpb, cta_warps)) {
     if (e == cudaSuccess) e = prep_ls_pair(method, smem);
   } else {
@@ -1078,7 +1080,7 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
       else if (ls_multi_supported(L, pair, wpb, cta_warps))
-        launch_ls_multi(L, D, method, wpb, smem, s);
+        launch_ls_multi(L, D, method, gen, s);
       else if (use_ls_pair(L, pair, wpb, cta_warps))
         launch_ls_pair(method, blocks_for((long long)D.R * D.L, wpb), 64 * wpb, smem, s, L, D);
       else

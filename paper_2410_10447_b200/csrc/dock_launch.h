@@ -62,14 +62,15 @@ cudaError_t launch_reduce7(const float* recs, int n, int n_red, int method, int 
 cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s);
 bool phase_prof_read(unsigned long long* out16, bool reset);
 bool phase_prof_read_multi(unsigned long long* out16, bool reset);  // adds ls_multi.cu's counters
+bool sm_searches_read(unsigned* out256, bool reset);  // searches per SM (phase-profiling builds)
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_sincos_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_dsqrt_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 
 // ls_multi.cu: the LGA's Lamarckian search on L.ls_warps warps per search
-bool ls_multi_supported(const LigandView& L, int pair, int poses, int cta_warps);
-cudaError_t prep_ls_multi(const LigandView& L, int method, size_t smem);
-void launch_ls_multi(const LigandView& L, const LgaDev& D, int method, int poses, size_t smem, cudaStream_t s);
+bool ls_multi_supported(const LigandView& L, int pair, int wpb, int cta_warps);
+cudaError_t prep_ls_multi(const LigandView& L, int method);
+void launch_ls_multi(const LigandView& L, const LgaDev& D, int method, int gen, cudaStream_t s);
 
 // bench_reduce.cu (C2 microbench)
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,

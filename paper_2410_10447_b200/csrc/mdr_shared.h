@@ -36,7 +36,7 @@ struct LigandView {
   int ls_warps;       // warps per Lamarckian search of the LGA (ls_multi.cu); 1 = the one-warp kernel
   int ls_n_chunks;    // site chunking of that search (its own lane count), see capi.cpp pick_chunks
   int ls_chunk_len;
-  int ls_stagger;     // cycles the odd searches of a launch start late (timing experiment; 0)
+  int pad_;
   int ls_group;       // atoms per chunk item of that search (register blocking: 1 or 3)
   const SiteD* sites;
   const double4* atoms;  // local x, y, z, weight
@@ -100,6 +100,7 @@ struct LgaDev {
   mdr_ls_record* recs;  // [R][maxrec]
   int* conv;        // [R]
   int* status;      // [R]
+  int* ls_next;     // [gens]: next search of generation g for the persistent search kernel (zeroed at init)
 };
 
 }  // namespace mdr

@@ -20,6 +20,8 @@ import bench
 from paper_2410_10447_b200 import Device, LgaSettings, SINGLE
 from paper_2410_10447_b200._lib import load
 lib = load(); dev = Device(0)
+import os
+if os.environ.get("AB_WPB"): assert lib.mdr_ctx_set_warps_per_block(dev.ctx, int(os.environ["AB_WPB"])) == 0
 s = torch.cuda.Stream(); torch.cuda.set_stream(s); dev.set_stream(s.cuda_stream)
 inst = bench.workload(); st = LgaSettings()
 di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))

@@ -102,7 +102,7 @@ def main():
             print(pname, name, out["lga"][f"{pname}/{name}"], flush=True)
         dev.close()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "parity_report.json"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", os.environ.get("PARITY_OUT", "parity_report.json")), "w") as f:
         json.dump(out, f, indent=1)
 
 

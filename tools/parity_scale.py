@@ -55,6 +55,9 @@ def main():
               "results": {}}
     modes = [("fp64", PAIR_FP64, BASELINE, SINGLE), ("fp64fast", PAIR_FP64_FAST, BASELINE, SINGLE),
              ("fp32", PAIR_FP32, BASELINE, SINGLE), ("fp64fast/tcu-half", PAIR_FP64_FAST, TCU, HALF)]
+    only = os.environ.get("PARITY_MODES")  # e.g. "fp64fast" (comma separated)
+    if only:
+        modes = [m for m in modes if m[0] in only.split(",")]
     for mname, pair, method, accum in modes:
         dev = Device(0, pair=pair)
         for name, inst in insts.items():
@@ -78,7 +81,7 @@ def main():
             print(mname, name, rec, flush=True)
         dev.close()
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "parity_scale.json"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", os.environ.get("PARITY_OUT", "parity_scale.json")), "w") as f:
         json.dump(report, f, indent=1)
 
 

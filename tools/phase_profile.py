@@ -34,9 +34,15 @@ def main():
     out = (C.c_uint64 * 16)()
     dev.lga_run_batch(c3(), BASELINE, SINGLE, LgaSettings(), seeds)  # warm
     assert lib.mdr_phase_prof(out, 1) == 0, lib.mdr_last_error(None)
+    sm = (C.c_uint32 * 256)()
+    lib.mdr_phase_prof_sm(sm, 1)
+    if os.environ.get("AB_WPB"):
+        assert lib.mdr_ctx_set_warps_per_block(dev.ctx, int(os.environ["AB_WPB"])) == 0
     dev.lga_run_batch(c3(), BASELINE, SINGLE, LgaSettings(), seeds)
     assert lib.mdr_phase_prof(out, 1) == 0
     v = list(out)
+    lib.mdr_phase_prof_sm(sm, 1)
+    per_sm = [x for x in sm][:148]
     ev = v[7]
     rep = {"evals": ev, "searches": v[11], "cycles_per_eval": {}}
     tot = sum(v[k] for k in range(7))
@@ -44,6 +50,12 @@ def main():
         if n:
             rep["cycles_per_eval"][n] = v[k] / ev
     rep["leader_total_per_eval"] = tot / ev
+    gens = LgaSettings().generations + 1  # LS launches per docking (generations + polish uses its own kernel)
+    hist = {}
+    for x in per_sm:
+        hist[x] = hist.get(x, 0) + 1
+    rep["searches_per_sm_per_docking"] = {"histogram (searches started on an SM over the docking: SM count)": hist,
+                                          "max": max(per_sm), "min": min(per_sm), "launches": gens}
     print(json.dumps(rep, indent=1))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", os.environ.get("PHASE_OUT", "phase_profile.json")), "w") as f:
