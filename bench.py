@@ -17,7 +17,7 @@ value    : device-resident (instance + seeds in HBM, CUDA graph of the whole
            before every timed step, max over ranks.
 e2e      : the same docking through the reference-facing host call
            mdr_lga_run_batch (host buffers; upload, graph build, run, download).
-roofline : the dominant kernel (lga_ls_kernel, the device ADADELTA chain)
+roofline : the dominant kernel (lga_ls_multi_kernel, the device ADADELTA chain)
            against the FP64 pipe (peak measured live by a DFMA kernel, see
            DESIGN.md §6).
 cpu_baseline : the reference library itself (oracle/_ref, compiled in place
@@ -246,7 +246,7 @@ def profiled_traffic():
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture of this configuration (profiles/, written on the box
     by tools/ncu_traffic.py), or None when absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_ls_kernel_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2_ls_kernel_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -452,7 +452,8 @@ def run_gpu_arm(args):
             flops = flop_per_eval(inst, settings.partition) * ls_evals.value
             achieved = flops / (ls_ms.value * 1e-3) / 1e12
             n_ls_launches = settings.generations + 1
-            roof = {"bound": "fp64", "kernel": "lga_ls_kernel / lga_ls_pair_kernel (device ADADELTA chain, warp (pair) per search)",
+            roof = {"bound": "fp64", "kernel": "lga_ls_multi_kernel (device ADADELTA chain, leader + helper warp per search, "
+                                               "persistent over each generation's searches)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": "measured live: DFMA-chain kernel on this GPU (MEASURED_PEAKS.json has no FP64 "
                                    "figure)",
