@@ -166,16 +166,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU arm
+def _cpu_workload(name):
+    """(instance, settings) of a named workload, for the CPU arm's workers."""
+    if name == "c4_analytic":
+        from paper_2410_10447_b200.workloads import c4_analytic
+
+        return c4_analytic()
+    return workload(), LgaSettings()
+
+
 def _cpu_worker(args):
     """One process: run LGA runs of the workload through the REFERENCE library
     (oracle/_ref) until `budget_s` elapsed; return (evals, seconds)."""
-    seeds, budget_s, kind = args
+    seeds, budget_s, kind, name = args
     sys.path.insert(0, ROOT)
     from oracle.oracle import Oracle
 
     o = Oracle(kind)
-    inst = workload()
-    s = LgaSettings()
+    inst, s = _cpu_workload(name)
     t0 = time.perf_counter()
     evals = runs = 0
     for sd in seeds:
@@ -187,7 +195,7 @@ def _cpu_worker(args):
     return evals, time.perf_counter() - t0, runs
 
 
-def cpu_measure(budget_s=12.0, procs=None):
+def cpu_measure(budget_s=12.0, procs=None, name="c3", seeds=None):
     import multiprocessing as mp
 
     from oracle.oracle import available, build
@@ -196,8 +204,8 @@ def cpu_measure(budget_s=12.0, procs=None):
     if kind == "port" and not available("port"):
         build()
     procs = procs or os.cpu_count() or 1
-    seeds = [int(x) for x in run_seeds(0)]  # the GPU arm's rank-0 seeds, cycled
-    jobs = [([seeds[(p + procs * k) % len(seeds)] for k in range(1000)], budget_s, kind) for p in range(procs)]
+    seeds = [int(x) for x in (run_seeds(0) if seeds is None else seeds)]  # the GPU arm's rank-0 seeds, cycled
+    jobs = [([seeds[(p + procs * k) % len(seeds)] for k in range(1000)], budget_s, kind, name) for p in range(procs)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(procs) as pool:
@@ -206,10 +214,12 @@ def cpu_measure(budget_s=12.0, procs=None):
     evals = sum(r[0] for r in res)
     runs = sum(r[2] for r in res)
     span = max(r[1] for r in res)
+    inst, s = _cpu_workload(name)
+    what = (f"the {name.upper().replace('_', ' ')} workload ({inst.n_atoms} atoms/{inst.n_rot} torsions/{inst.n_sites} "
+            f"sites, partition {s.partition}")
     return {"value": evals / span, "unit": UNIT, "cores": procs, "kind": kind,
-            "sample": f"{runs} LGA runs of the C3 workload ({N_ATOMS} atoms/{N_ROT} torsions/{N_SITES} sites, "
-                      f"default LgaSettings, Baseline reduction, the GPU arm's seeds 1000000.. cycled) on {procs} "
-                      f"processes x ~{budget_s:.0f} s; {evals} evaluations", "wall_s": wall,
+            "sample": f"{runs} LGA runs of {what}, default LgaSettings otherwise, Baseline reduction, the GPU arm's "
+                      f"seeds cycled) on {procs} processes x ~{budget_s:.0f} s; {evals} evaluations", "wall_s": wall,
             "cpu_model": cpu_model(), "nproc": os.cpu_count(),
             "build": "oracle/_ref: reference sources, g++ -std=c++20 -O3 -DNDEBUG -ffp-contract=off (its Release flags)"}
 
@@ -537,6 +547,86 @@ def mode_sweep(lib, torch, local, inst, settings, steps=3):
     return out
 
 
+def c4_analytic_measure(lib, torch, local, steps=5, runs=N_RUNS, cpu_seconds=12.0):
+    """C4 in the reference's own scoring (BASELINE.json configs[3] ligand:
+    100 atoms / 30 torsions, 64 analytic sites, partition 128, 100 LGA runs):
+    device-resident evals/s, the host-buffer call, the dominant kernel's
+    roofline and the reference library on this host's cores -- a second
+    reference-pinned configuration next to C3."""
+    from paper_2410_10447_b200 import Device
+    from paper_2410_10447_b200.workloads import c4_analytic
+
+    inst, settings = c4_analytic()
+    stream = torch.cuda.current_stream()
+    seeds_host = np.arange(runs, dtype=np.uint64) + np.uint64(3_000_000)
+    seeds = torch.from_numpy(seeds_host.view(np.int64)).to(f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    dev = Device(local)
+    dev.set_stream(stream.cuda_stream)
+    di = lib.mdr_instance_upload(dev.ctx, C.byref(inst.c()))
+    b = lib.mdr_lga_batch_create(dev.ctx, di, BASELINE, SINGLE, C.byref(settings), runs)
+    assert b, lib.mdr_last_error(dev.ctx)
+    tot = torch.zeros(1, dtype=torch.int64, device=f"cuda:{local}")
+    for _ in range(3):
+        lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+    lib.mdr_lga_batch_total_evals_dev(dev.ctx, b, C.c_void_p(tot.data_ptr()))
+    torch.cuda.synchronize()
+    ev = int(tot.item())
+    ms = []
+    for k in range(steps):
+        flush.fill_(float(k))
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        lib.mdr_lga_batch_run_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()))
+        e.record(stream)
+        e.synchronize()
+        ms.append(a.elapsed_time(e))
+    t = statistics.median(ms)
+    ls_ms, all_ms, ls_ev = C.c_float(), C.c_float(), C.c_int64()
+    lib.mdr_lga_batch_profile_dev(dev.ctx, b, C.c_void_p(seeds.data_ptr()), C.byref(ls_ms), C.byref(all_ms),
+                                  C.byref(ls_ev))
+    fl = flop_per_eval(inst, settings.partition)
+    peak = fp64_peak_tflops(torch)
+    ach = fl * ls_ev.value / (ls_ms.value * 1e-3) / 1e12 if ls_ms.value else None
+    # the same docking through the reference-facing host call
+    dim = inst.dim
+    be, bg = np.zeros(runs), np.zeros((runs, dim))
+    evs, cv, nr = np.zeros(runs, np.int64), np.zeros(runs, np.int32), np.zeros(runs, np.int32)
+    recs = (LsRecord * (runs * settings.max_records))()
+    st = (SyncStats * runs)()
+    pinned = torch.from_numpy(seeds_host.view(np.int64)).pin_memory()
+
+    def e2e_call():
+        rc = lib.mdr_lga_run_batch(dev.ctx, C.byref(inst.c()), BASELINE, SINGLE, C.byref(settings),
+                                   C.c_void_p(pinned.data_ptr()), runs, be.ctypes.data, bg.ctypes.data, evs.ctypes.data,
+                                   cv.ctypes.data, nr.ctypes.data, recs, st)
+        assert rc == 0, lib.mdr_last_error(dev.ctx)
+
+    e2e_call()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        e2e_call()
+    e2e = int(evs.sum()) * 3 / (time.perf_counter() - t0)
+    lib.mdr_lga_batch_destroy(dev.ctx, b)
+    lib.mdr_instance_free(dev.ctx, di)
+    dev.close()
+    out = {"workload": f"C4 analytic: {inst.n_atoms} atoms / {inst.n_rot} torsions / {inst.n_sites} sites, partition "
+                       f"{settings.partition}, {runs} LGA runs, default LgaSettings otherwise (BASELINE.json configs[3] "
+                       "ligand in the reference's own scoring)",
+           "evals_per_s": ev / (t * 1e-3), "ms_per_step": t, "evals_per_step": ev,
+           "docking_sec_per_ligand": t * 1e-3, "l2": "flushed (256 MB write) before every step",
+           "e2e": {"value": e2e, "unit": UNIT, "api": "mdr_lga_run_batch (host buffers)"},
+           "roofline": {"bound": "fp64", "kernel": "LGA local-search kernel", "achieved": ach, "peak": peak,
+                        "unit": "TFLOP/s", "frac": (ach or 0.0) / peak, "flop_per_eval": fl,
+                        "ls_kernel_share": ls_ms.value / all_ms.value if all_ms.value else None}}
+    if cpu_seconds > 0:
+        cpu = cpu_measure(cpu_seconds, name="c4_analytic", seeds=seeds_host)
+        out["cpu_baseline"] = cpu
+        out["vs_reference"] = {"ratio": out["evals_per_s"] / cpu["value"], "e2e_ratio": e2e / cpu["value"]}
+    return out
+
+
 def grid_flop_bytes_per_eval(inst, params, partition):
     """Algorithmic work of one grid-mode evaluation:
     bytes = atoms x 8 corners x 3 maps x 4 B (the gathered map values);
@@ -737,12 +827,48 @@ def extra_measurements(args, dev, lib, torch):
     microbench (ns/call)."""
     out = {"modes": mode_sweep(lib, torch, torch.cuda.current_device(), workload(), LgaSettings())}
     out["score_kernel"] = score_throughput(lib, torch, torch.cuda.current_device())
+    out["c4_analytic"] = c4_analytic_measure(lib, torch, torch.cuda.current_device(),
+                                             cpu_seconds=0.0 if args.no_cpu else args.cpu_seconds)
     out["c4_grid"] = c4_measure(lib, torch, torch.cuda.current_device())
     out["c5_screen"] = c5_measure(torch, torch.cuda.current_device())
     if hasattr(lib, "mdr_reduce_bench_dev"):
-        from paper_2410_10447_b200.microbench import reduce_microbench
+        from paper_2410_10447_b200.microbench import cpu_leg, reduce_microbench
 
-        out["reduce_microbench"] = reduce_microbench(dev, lib, torch)
+        mb = reduce_microbench(dev, lib, torch)
+        if not args.no_cpu:
+            mb["cpu_leg"] = cpu_leg()
+        out["reduce_microbench"] = mb
+        out["c2_float4_block_reduce"] = c2_summary(mb)
+    return out
+
+
+def c2_summary(mb):
+    """BASELINE.json metric "float4 block-reduce ns/call" (configs[1]) per
+    block size: the fastest fp32-accurate shuffle kernel, the paper's f16
+    MMA, the error-compensated MMAs (warp mma.sync and the batched tcgen05
+    contraction the library routes TcuSplit batches to), and the reference
+    library on this host's CPU (one core, and all cores)."""
+    out = {"unit": "ns/call", "timing": "GPU: 10^6 reductions per launch (ns per reduction of the whole GPU); "
+                                        "latency: clock64 cycles per dependent step of one block", "blocks": {}}
+    for B, res in mb["results"].items():
+        row = {}
+        for k in ("shuffle_2level (K1c)", "wmma_f16 (paper, K2)", "split_tf32_warp (K2s)",
+                  "tcgen05_batched_tf32x2 (K2t)"):
+            r = res.get(k, {})
+            row[k] = {"chain_ns": r.get("chain_ns"), "stream_ns": r.get("stream_ns"),
+                      "latency_ns_per_step": (r.get("latency") or {}).get("ns_per_step"),
+                      "chain_smem_frac": (r.get("chain_roofline") or {}).get("frac"),
+                      "stream_hbm_frac": (r.get("stream_roofline") or {}).get("frac")}
+        prod = mb.get("product", {}).get(B, {})
+        row["library reduce4 TcuSplit"] = prod.get("reduce4 TcuSplit (tcgen05 route)")
+        cpu = mb.get("cpu_leg", {}).get("results", {}).get(B, {})
+        if cpu:
+            row["cpu reference reduce4 Tcu f16"] = cpu.get("reduce4 Tcu f16 (Half)")
+            row["cpu reference simulate_block Baseline"] = cpu.get("simulate_block Baseline (4 block trees)")
+        out["blocks"][B] = row
+    cpu = mb.get("cpu_leg", {})
+    if cpu.get("cores"):
+        out["cpu"] = {"cores": cpu["cores"], "model": cpu.get("cpu_model"), "kind": cpu.get("kind")}
     return out
 
 

@@ -219,10 +219,20 @@ int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches);
  * steps on one input set (d_in: blocks x block x 4 floats); chain_steps == 0:
  * n_red distinct input sets streamed from HBM.  d_out: one float4 per block
  * (chain) or per reduction (stream).  Device pointers, enqueue only. */
+/* C2 inputs, device-generated and offset-addressable:
+ * d_out[i] = (float) uniform(-1, 1) of draw i + 1 of derive_rng(seed, label)
+ * (rng.hpp:41-43), the values the reference's RngStream yields on the host.
+ * Enqueue only. */
+int mdr_fill_uniform_dev(mdr_ctx* ctx, uint64_t seed, const char* label, int64_t n, float* d_out);
 int mdr_reduce_bench_kernels(void);
 const char* mdr_reduce_bench_kernel_name(int kernel);
 int mdr_reduce_bench_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in,
                          int n_red, int chain_steps, float* d_out);
+/* Chain mode of mdr_reduce_bench_dev that also writes, per block, the SM
+ * clock cycles of its whole dependent chain (d_cycles: n_red / chain_steps
+ * int64): the latency metric, cycles per reduce-and-broadcast step. */
+int mdr_reduce_bench_chain_cycles_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in, int n_red,
+                                      int chain_steps, float* d_out, int64_t* d_cycles);
 
 /* ---- L2 scoring (docking.hpp:44-63) ------------------------------------ */
 /* score docking.cpp:191-233 for n genotypes (n x dim, dim = 6 + n_rot,

@@ -5,6 +5,7 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's CPU arm may load it.
 // Every function forwards to the reference's own C++ API (namespace mdreduce)
 // and converts its exceptions into the status codes of include/mdr.h.
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -362,6 +363,78 @@ int ref_write_results(int n, const uint64_t* seed, const char* const* method, co
         const size_t k = s.size() < cap ? s.size() : cap - 1;
         std::memcpy(out, s.data(), k);
         out[k] = 0;
+    });
+}
+
+// ---- C2 CPU leg (test / bench infrastructure): the reference's own
+// reduction calls timed in a loop, like cli.cpp:195-266 (cmd_reduce_bench).
+
+// out[i] = (float) uniform(-1, 1) of draw i + 1 of derive_rng(seed, label)
+// (rng.hpp:41-43, rng.cpp:43-45): the C2 inputs, identical to
+// the device generator's.
+int ref_fill_uniform(uint64_t seed, const char* label, int64_t n, float* out) {
+    return guarded([&] {
+        RngStream rng = derive_rng(seed, label);
+        for (int64_t i = 0; i < n; ++i) out[i] = static_cast<float>(rng.uniform(-1.0, 1.0));
+    });
+}
+
+// Calls of one reduction over the n_red input sets of B records (cycled)
+// until budget_s elapsed; *ns_per_call = wall time / calls.
+//   kind 0: reduce4 (reduce.cpp:80-111; in = n_red x B x 4) with
+//           method TCU, or simulate_block's baseline four block reductions
+//           (simblock.cpp) with method BASELINE;
+//   kind 1: reduce7 (reduce.cpp:165-209; in = n_red x B x 7), either method;
+//   kind 2: baseline_block_reduce (reduce.cpp:136-163; in = n_red x B).
+int ref_time_reduce(int kind, int method, int accum, int B, const float* in, int n_red, double budget_s,
+                    double* ns_per_call, double* checksum, int64_t* calls) {
+    return guarded([&] {
+        const int comps = kind == 0 ? 4 : (kind == 1 ? 7 : 1);
+        std::vector<std::vector<Vec4>> v4;
+        std::vector<std::vector<Partial7>> v7;
+        for (int r = 0; r < n_red; ++r) {
+            const float* p = in + static_cast<size_t>(r) * B * comps;
+            if (kind == 0) {
+                std::vector<Vec4> v(static_cast<size_t>(B));
+                for (int t = 0; t < B; ++t) v[t] = Vec4{p[4 * t], p[4 * t + 1], p[4 * t + 2], p[4 * t + 3]};
+                v4.push_back(std::move(v));
+            } else if (kind == 1) {
+                std::vector<Partial7> v(static_cast<size_t>(B));
+                for (int t = 0; t < B; ++t)
+                    v[t] = Partial7{p[7 * t], p[7 * t + 1], p[7 * t + 2], p[7 * t + 3], p[7 * t + 4], p[7 * t + 5],
+                                    p[7 * t + 6]};
+                v7.push_back(std::move(v));
+            }
+        }
+        const BlockConfig cfg(B, meth(method), acc(accum));
+        double sum = 0.0;
+        int64_t n = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        double el = 0.0;
+        do {
+            for (int r = 0; r < n_red; ++r, ++n) {
+                if (kind == 0) {
+                    if (method == MDR_METHOD_TCU) {
+                        auto [x, st] = reduce4(v4[r], acc(accum));
+                        sum += x.x;
+                    } else {
+                        auto [x, st] = simulate_block(cfg, std::span<const Vec4>(v4[r]));
+                        sum += x.x;
+                    }
+                } else if (kind == 1) {
+                    auto [x, st] = reduce7(v7[r], meth(method), acc(accum));
+                    sum += x[0];
+                } else {
+                    auto [x, st] = baseline_block_reduce(
+                        std::span<const float>(in + static_cast<size_t>(r) * B, static_cast<size_t>(B)), B);
+                    sum += x;
+                }
+            }
+            el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        } while (el < budget_s);
+        *ns_per_call = el * 1e9 / static_cast<double>(n);
+        *checksum = sum;
+        *calls = n;
     });
 }
 

@@ -73,6 +73,8 @@ _SIGS = {
     "mdr_selftest_sincos": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_crmath": (I, [P, C.c_int64, P]),
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
+    "mdr_fill_uniform_dev": (I, [P, U64, C.c_char_p, C.c_int64, P]),
+    "mdr_reduce_bench_chain_cycles_dev": (I, [P, I, I, P, I, I, P, P]),
     "mdr_reduce_bench_kernels": (I, []),
     "mdr_reduce_bench_kernel_name": (C.c_char_p, [I]),
     "mdr_grid_upload": (P, [P, P]),

@@ -318,18 +318,27 @@ __device__ __forceinline__ float4 reduce_once(float4 v, Smem& sm, int it) {
   return k2b(v, sm, it);
 }
 
+// cyc (optional): per block, the SM clock cycles of its whole chain
+// (clock64 by thread 0 around the loop, after a block barrier), for the
+// latency metric (cycles per dependent step).
 template <int K>
-__global__ void chain_kernel(const float4* __restrict__ in, int steps, float4* __restrict__ out) {
+__global__ void chain_kernel(const float4* __restrict__ in, int steps, float4* __restrict__ out,
+                             long long* __restrict__ cyc) {
   __shared__ Smem sm;
   sm.tile = reinterpret_cast<__half*>(g_dyn);
   sm.stage = reinterpret_cast<float*>(g_dyn);
   float4 v = in[(size_t)blockIdx.x * blockDim.x + threadIdx.x];
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  const long long t0 = clock64();
   for (int it = 0; it < steps; ++it) {
     s = reduce_once<K>(v, sm, it);
     v = add_feed(v, s);
   }
-  if (threadIdx.x == 0) out[blockIdx.x] = s;
+  if (threadIdx.x == 0) {
+    out[blockIdx.x] = s;
+    if (cyc) cyc[blockIdx.x] = clock64() - t0;
+  }
 }
 
 template <int K>
@@ -353,7 +362,7 @@ static const char* kNames[] = {"reducefs_x4 (AutoDock, K1a)", "shuffle_transpose
                                "tcgen05_tma_pipelined (K2t2)"};
 
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
-                                int blocks_per_sm, cudaStream_t s) {
+                                int blocks_per_sm, cudaStream_t s, long long* cycles) {
   const float4* i4 = reinterpret_cast<const float4*>(in);
   float4* o4 = reinterpret_cast<float4*>(out);
   const size_t dyn = kernel == 2 ? (size_t)8 * block
@@ -361,7 +370,7 @@ cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_re
                      : (kernel == 3 || kernel == 4) ? (size_t)16 * block : 0;
   if (chain_steps > 0) {
     const int grid = n_red / chain_steps;
-#define CH(K) bench::chain_kernel<K><<<grid, block, dyn, s>>>(i4, chain_steps, o4)
+#define CH(K) bench::chain_kernel<K><<<grid, block, dyn, s>>>(i4, chain_steps, o4, cycles)
     switch (kernel) {
       case 0: CH(0); break;
       case 1: CH(1); break;

@@ -708,6 +708,19 @@ int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches) {
   return MDR_OK;
 }
 
+int mdr_reduce_bench_chain_cycles_dev(mdr_ctx* ctx, int kernel, int block, const float* d_in, int n_red,
+                                      int chain_steps, float* d_out, int64_t* d_cycles) {
+  if (!ctx || !d_in || !d_out || !d_cycles || n_red <= 0 || chain_steps <= 0 || kernel < 0 || kernel >= 7)
+    return fail(ctx, MDR_ERR_INVALID, "bad argument (chain-mode kernels 0..6)");
+  if (block < 64 || block > 1024 || block % 64)
+    return fail(ctx, MDR_ERR_BLOCK_SIZE, "bench blocks are multiples of 64 in [64, 1024]");
+  if (n_red % chain_steps) return fail(ctx, MDR_ERR_SIZE, "n_red must be a multiple of steps");
+  CK(launch_reduce_bench(kernel, block, d_in, n_red, chain_steps, d_out, 0, ctx->stream,
+                         reinterpret_cast<long long*>(d_cycles)));
+  ctx->launches++;
+  return MDR_OK;
+}
+
 int mdr_reduce_bench_kernels(void) { return kReduceBenchKernels; }
 const char* mdr_reduce_bench_kernel_name(int k) { return reduce_bench_name(k); }
 
@@ -1126,6 +1139,13 @@ static uint64_t label_hash(const char* label) {  // mix64(fnv1a64(label)), rng.c
   uint64_t h = 0xcbf29ce484222325ull;
   for (const unsigned char* p = reinterpret_cast<const unsigned char*>(label); *p; ++p) h = (h ^ *p) * 0x100000001b3ull;
   return mix64_host(h);
+}
+
+int mdr_fill_uniform_dev(mdr_ctx* ctx, uint64_t seed, const char* label, int64_t n, float* d_out) {
+  if (!ctx || !label || n < 0 || (n && !d_out)) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  CK(launch_fill_uniform(mix64_host(seed ^ label_hash(label)), (long long)n, d_out, S(ctx)));  // rng.cpp:31-32
+  ctx->launches++;
+  return MDR_OK;
 }
 
 static int check_lga(mdr_ctx* ctx, int method, const mdr_lga_settings* s) {

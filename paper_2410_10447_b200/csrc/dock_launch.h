@@ -63,6 +63,7 @@ cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s
 bool phase_prof_read(unsigned long long* out16, bool reset);
 bool phase_prof_read_multi(unsigned long long* out16, bool reset);  // adds ls_multi.cu's counters
 bool sm_searches_read(unsigned* out256, bool reset);  // searches per SM (phase-profiling builds)
+cudaError_t launch_fill_uniform(uint64_t key, long long n, float* out, cudaStream_t s);
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_sincos_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_dsqrt_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
@@ -74,7 +75,7 @@ void launch_ls_multi(const LigandView& L, const LgaDev& D, int method, int gen, 
 
 // bench_reduce.cu (C2 microbench)
 cudaError_t launch_reduce_bench(int kernel, int block, const float* in, int n_red, int chain_steps, float* out,
-                                int blocks_per_sm, cudaStream_t s);
+                                int blocks_per_sm, cudaStream_t s, long long* cycles = nullptr);
 const char* reduce_bench_name(int k);
 constexpr int kReduceBenchKernels = 9;  // ids 7, 8 = tcgen05 batched (stream mode only; 8 = TMA-fed)
 

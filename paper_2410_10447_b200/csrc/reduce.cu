@@ -200,6 +200,14 @@ __global__ void reduce7_kernel(const float* __restrict__ recs, int n, int n_red,
   }
 }
 
+// ------------------------------------------------------- C2 bench inputs
+// out[i] = (float) uniform(-1, 1) of draw i + 1 of the stream with key `key`
+// (RngStream::uniform rng.cpp:43-45: lo + (hi - lo) * next_double()).
+__global__ void fill_uniform_kernel(uint64_t key, long long n, float* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = (float)(-1.0 + 2.0 * draw_unit(key, (uint64_t)i + 1));
+}
+
 // ------------------------------------------------------------ self test
 // ddiv_rn (branch-free division) against the compiler's IEEE div.rn.f64 on
 // counter-generated operands: numerators log-uniform over [2^-40, 2^40]
@@ -218,6 +226,12 @@ __global__ void ddiv_selftest_kernel(uint64_t seed, long long n, unsigned long l
 }
 
 // ------------------------------------------------------------ launchers
+cudaError_t launch_fill_uniform(uint64_t key, long long n, float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  fill_uniform_kernel<<<148 * 8, 256, 0, s>>>(key, n, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s) {
   ddiv_selftest_kernel<<<148 * 8, 256, 0, s>>>(seed, n, mismatches);
   return cudaGetLastError();

@@ -4,9 +4,11 @@ reference's counter RNG (derive_rng, rng.hpp:41-43) and its random_instance
 recipe (tests/test_docking.cpp:39-59), so CPU and GPU see identical inputs.
 
   C3  small ligand: 20 atoms, 5 torsions, 64 analytic sites   ("synth/small")
-  C4  large flexible ligand: 100 atoms, 30 torsions, grid mode on 126^3 maps
-      at 0.375 A (4 atom types + electrostatic + desolvation), sampled from 64
-      sites by mdr_grid_build; intramolecular pairs on    ("synth/large")
+  C4  large flexible ligand: 100 atoms, 30 torsions ("synth/large"), in two
+      forms: analytic (the reference's scoring against its 64 sites,
+      partition 128) and grid mode on 126^3 maps at 0.375 A (4 atom types +
+      electrostatic + desolvation), sampled from the 64 sites by
+      mdr_grid_build; intramolecular pairs on
   C5  virtual screen: ligand j has U[10,100] atoms and U[0,30] torsions
       ("synth/lig/<j>") against the C4 receptor
 """
@@ -29,6 +31,15 @@ def c3():
     inst = random_instance(derive_rng(SEED, "synth/small"), 5, 20, 64)
     inst.name = "synth/small"
     return inst
+
+
+def c4_analytic():
+    """C4 in the reference's own (analytic) scoring: the C4 ligand (100 atoms,
+    30 torsions) against its 64 sites, partition 128, so the
+    reference library itself can dock it (docking.cpp:392-517)."""
+    inst = random_instance(derive_rng(SEED, "synth/large"), 30, 100, 64)
+    inst.name = "synth/large"
+    return inst, LgaSettings(partition=128)
 
 
 def c4_receptor(n: int = 126, spacing: float = 0.375, n_sites: int = 64):

@@ -121,3 +121,31 @@ def test_fp32_mode_c3_fenced(c3_reference):
     assert same <= 20  # divergent trajectories: the mode is NOT a per-run reproduction
     assert abs(welch) < 3.0, welch
     assert np.all(np.isfinite(g)) and g.min() < -100.0
+
+
+# ---- C4 analytic (BASELINE.json configs[3] ligand in the reference's own
+# scoring; bench.py c4_analytic): 100 atoms, 30 torsions, 64 sites,
+# partition 128.  48 paired seeds of bench.py's C4 seeds (3 000 000 + i).
+C4A_SEEDS = np.arange(48, dtype=np.uint64) + np.uint64(3_000_000)
+
+
+def test_c4_analytic_against_reference(dev, port, ref):
+    """Device LGA runs of C4 analytic against the reference library on the
+    same seeds: >= 90 % identical runs (best energy and evaluation count),
+    mean best energies within the reference's 0.2 % gate
+    (acceptance.cpp:128-145), identical 2 A clusters of the final poses."""
+    from oracle.oracle import lga_runs_parallel
+    from paper_2410_10447_b200.workloads import c4_analytic
+
+    inst, s = c4_analytic()
+    cpu = lga_runs_parallel("reference", inst, BASELINE, SINGLE, s, C4A_SEEDS)
+    gpu = dev.lga_run_batch(inst, BASELINE, SINGLE, c4_analytic()[1], C4A_SEEDS)
+    same = sum(g.best_energy == r[0] and g.evaluations == r[1] for g, r in zip(gpu, cpu))
+    ge = np.array([g.best_energy for g in gpu])
+    re = np.array([r[0] for r in cpu])
+    print(f"c4 analytic: identical {same}/{len(gpu)}, means {ge.mean():.4f} vs {re.mean():.4f}")
+    assert same >= 0.9 * len(gpu), same
+    assert abs(ge.mean() - re.mean()) / abs(re.mean()) < 2e-3
+    gc, _, gn = dev.cluster_poses(inst, np.stack([g.best_genotype for g in gpu]), ge, 2.0)
+    rc, _, rn = port.cluster_poses(inst, np.stack([r[3] for r in cpu]), re, 2.0)
+    assert gn == rn and np.array_equal(gc, rc), (gn, rn)

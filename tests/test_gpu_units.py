@@ -227,3 +227,20 @@ def test_reduce7_split_tcgen05_route(dev, n):
     ri = rng.integers(0, 2, (n_red, n, 7)).astype(np.float32)
     got, _ = dev.reduce7_batch(ri, TCU_SPLIT, SINGLE)
     assert np.array_equal(got, ri.sum(1))
+
+
+def test_c2_device_inputs_equal_reference_stream(dev, ref):
+    """mdr_fill_uniform_dev (the C2 microbench's device-generated inputs)
+    equals the reference's RngStream::uniform(-1, 1) draw for draw."""
+    import ctypes as C
+
+    import torch
+
+    n = 100_003
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    assert dev.lib.mdr_fill_uniform_dev(dev.ctx, 12345, b"bench/128/float4", n, C.c_void_p(x.data_ptr())) == 0
+    torch.cuda.synchronize()
+    want = np.empty(n, np.float32)
+    ref.lib.ref_fill_uniform.argtypes = [C.c_uint64, C.c_char_p, C.c_int64, C.c_void_p]
+    assert ref.lib.ref_fill_uniform(12345, b"bench/128/float4", n, want.ctypes.data) == 0
+    assert np.array_equal(x.cpu().numpy().view(np.uint32), want.view(np.uint32))

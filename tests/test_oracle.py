@@ -306,3 +306,32 @@ def test_lga_random_vs_reference(port, ref, instances):
             y = ref.lga_run(instances["s3"], m, a, s, 1000 + seed)
             assert x["best_energy"] == y["best_energy"] and x["evaluations"] == y["evaluations"]
             assert np.array_equal(x["best_genotype"], y["best_genotype"]) and x["runs"] == y["runs"]
+
+
+def test_c2_bench_inputs_are_the_reference_stream(ref):
+    """The C2 microbench inputs: ref_fill_uniform (the
+    reference's RngStream::uniform(-1, 1), rng.cpp:43-45) equals the Python
+    mirror draw for draw; the device generator is pinned to the same shim in
+    tests/test_gpu_units.py."""
+    import ctypes as C
+
+    from paper_2410_10447_b200._abi import derive_rng
+
+    n = 257
+    x = np.empty(n, np.float32)
+    ref.lib.ref_fill_uniform.argtypes = [C.c_uint64, C.c_char_p, C.c_int64, C.c_void_p]
+    assert ref.lib.ref_fill_uniform(12345, b"bench/64/float4", n, x.ctypes.data) == 0
+    rng = derive_rng(12345, "bench/64/float4")
+    want = np.array([rng.uniform(-1.0, 1.0) for _ in range(n)], np.float32)
+    assert np.array_equal(x.view(np.uint32), want.view(np.uint32))
+
+
+def test_c2_cpu_leg_times_the_reference(ref):
+    """The CPU leg of the C2 microbench runs the reference's own reduce4 /
+    simulate_block / reduce7 / baseline_block_reduce (ref_time_reduce)."""
+    from paper_2410_10447_b200.microbench import cpu_leg
+
+    out = cpu_leg(blocks=(64,), n_sample=8, budget_s=0.05, procs=2)
+    row = out["results"]["64"]
+    assert len(row) == 5 and all(v["ns_per_call_1core"] > 0 and v["calls_all_cores"] > 0 for v in row.values())
+    assert out["kind"] == "reference" and out["cores"] == 2
