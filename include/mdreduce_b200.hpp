@@ -356,9 +356,12 @@ void set_device(int device);
 //               correctly rounded trig (399/400 paired LGA runs identical);
 //   Fast64    — FP64 with FMA and one reciprocal per pair (default; float
 //               outputs bit-identical to the reference on every measured
-//               evaluation and local search, 380/400 paired LGA runs,
-//               profiles/r1_parity_scale.json);
-//   Fp32      — FP32 pair terms (within 1e-5 relative, fastest).
+//               evaluation and local search, 382/400 paired LGA runs,
+//               profiles/r2_rcp_parity.json);
+//   Fp32      — FP32 pair terms: per evaluation within 1e-5 relative, but LGA
+//               trajectories diverge from the reference and C3's paired-seed
+//               means miss the reference's 0.2 % gate (6.7e-3): statistical
+//               parity only, not for reference reproduction.
 enum class PairMode { Reference, Fast64, Fp32 };
 void set_pair_mode(PairMode mode);
 // Torsion gradient of the analytic path (per thread; see mdr_ctx_set_exact_torsion):

@@ -261,8 +261,11 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
   if (bad_out) return out;
   // B: frame (reference product order Rz(phi) Ry(theta) Rz(alpha)), atoms
   const double2 t1 = trig[0], t2 = trig[1], t3 = trig[2];
-  const Frame fr = frame_from_trig(t1.x, t1.y, t2.x, t2.y, t3.x, t3.y);
-  const m3& R = fr.R;
+  const m3 rz1 = {{t1.y, -t1.x, 0.0, t1.x, t1.y, 0.0, 0.0, 0.0, 1.0}};
+  const m3 ry2 = {{t2.y, 0.0, t2.x, 0.0, 1.0, 0.0, -t2.x, 0.0, t2.y}};
+  const m3 rz3 = {{t3.y, -t3.x, 0.0, t3.x, t3.y, 0.0, 0.0, 0.0, 1.0}};
+  const m3 ab = mm(rz1, ry2);
+  const m3 R = mm(ab, rz3);
   const double tx = S.g[0], ty = S.g[1], tz = S.g[2];
   float rec[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int i = tid; i < S.na; i += T) {
@@ -358,9 +361,9 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
       if (tid == 3)
         ax = {0.0, 0.0, 1.0};
       else if (tid == 4)
-        ax = fr.ax_theta;
+        ax = mv(rz1, d3{0.0, 1.0, 0.0});
       else
-        ax = fr.ax_alpha;
+        ax = mv(ab, d3{0.0, 0.0, 1.0});
       out.gd = (float)ax.x * sums[4] + (float)ax.y * sums[5] + (float)ax.z * sums[6];
     } else {
       const int k = tid - 6, C = S.C;
