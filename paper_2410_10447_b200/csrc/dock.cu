@@ -673,8 +673,8 @@ __global__ void lga_init_finalize(LgaDev D) {
     D.status[run] = MDR_OK;
     D.active[run] = D.gens > 0 && budget_ok(D, D.P);
   }
-  if (run == 0)  // work counters of the persistent search kernel, one per generation
-    for (int g = lane; g < D.gens; g += 32) D.ls_next[g] = 0;
+  if (run == 0)  // work counters of the persistent search kernel: one per generation, one for the polish
+    for (int g = lane; g <= D.gens; g += 32) D.ls_next[g] = 0;
 }
 
 // Bookkeeping of one generation, warp per run, with the reference's
@@ -1031,6 +1031,19 @@ static void launch_ls_pair(int method, int blocks, int threads, size_t smem, cud
 #ifndef MDR_POLISH_CTA
 #define MDR_POLISH_CTA 4  // measured: 0 / 2 / 4 / 8 -> 139.3 / 139.4 / 141.3 / 141.3 M evals/s on C3
 #endif
+// The final polish: on the two-warp persistent search when the searches run
+// there; otherwise, for ligands that would qualify for it (A/B contexts:
+// MDR_LS_WARPS 0 or 1), on the one-warp search kernel, so every search
+// configuration gives bit-identical dockings; else the CTA-per-pose polish.
+static bool polish_multi(const LigandView& L, int pair, int wpb, int cta_warps) {
+  return ls_multi_supported(L, pair, wpb, cta_warps);
+}
+static bool polish_one_warp(const LigandView& L, int pair, int wpb, int cta_warps) {
+  LigandView M = L;
+  M.ls_pair = 1;
+  M.ls_warps = 2;
+  return !polish_multi(L, pair, wpb, cta_warps) && ls_multi_supported(M, pair, wpb, cta_warps);
+}
 static int polish_warps(const LigandView& L, int pair, int cta_warps) {
   if (L.exact_torsion) return 0;  // exact-torsion staging lives in the warp-per-pose region
   return cta_warps > 0 ? cta_warps : (pair != MDR_PAIR_FP64 ? MDR_POLISH_CTA : 0);
@@ -1038,7 +1051,9 @@ static int polish_warps(const LigandView& L, int pair, int cta_warps) {
 
 cudaError_t prepare_lga(const LigandView& L, int method, int pair, int wpb, int cta_warps) {
   const size_t smem = warp_smem(L, wpb);
-  const int pw = polish_warps(L, pair, cta_warps);
+  const int pw = polish_multi(L, pair, wpb, cta_warps) || polish_one_warp(L, pair, wpb, cta_warps)
+                     ? 0
+                     : polish_warps(L, pair, cta_warps);
   cudaError_t e = prep_lga_init_kernel(method, pair, L, smem);
   if (e == cudaSuccess) e = prep_lga_offspring_kernel(method, pair, L, smem);
   if (cta_warps > 0) {
@@ -1091,11 +1106,20 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
     launches += D.L > 0 ? 3 : 2;
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
-  const int pw = polish_warps(L, pair, cta_warps);
-  if (pw > 0)
-    dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * pw, cta_smem(L, pw), s, L, D);
-  else
-    dispatch_lga_polish_kernel(method, pair, L, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
+  if (polish_multi(L, pair, wpb, cta_warps)) {
+    launch_ls_multi(L, D, method, D.gens, s);
+  } else if (polish_one_warp(L, pair, wpb, cta_warps)) {
+    LigandView P = L;  // the search's own chunking, as the two-warp polish would use
+    P.n_chunks = L.ls_n_chunks;
+    P.chunk_len = L.ls_chunk_len;
+    dispatch_lga_polish_kernel(method, pair, P, blocks_for(D.R, wpb), 32 * wpb, smem, s, P, D);
+  } else {
+    const int pw = polish_warps(L, pair, cta_warps);
+    if (pw > 0)
+      dispatch_lga_polish_cta_kernel(method, pair, D.R, 32 * pw, cta_smem(L, pw), s, L, D);
+    else
+      dispatch_lga_polish_kernel(method, pair, L, blocks_for(D.R, wpb), 32 * wpb, smem, s, L, D);
+  }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 1], s);
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens + 3], s);
   launches += 1;

@@ -100,7 +100,7 @@ struct LgaDev {
   mdr_ls_record* recs;  // [R][maxrec]
   int* conv;        // [R]
   int* status;      // [R]
-  int* ls_next;     // [gens]: next search of generation g for the persistent search kernel (zeroed at init)
+  int* ls_next;     // [gens + 1]: next search of generation g / next polish ([gens]) for the persistent search kernel (zeroed at init)
 };
 
 }  // namespace mdr
