@@ -715,7 +715,7 @@ def c4_measure(lib, torch, local, methods=("baseline", "split", "tcu"), partitio
     return out
 
 
-def c5_measure(torch, local, n_ligands=10_000, runs=10, method="baseline", batch=256):
+def c5_measure(torch, local, n_ligands=10_000, runs=10, method="baseline", batch=1024):
     """C5 (BASELINE.json configs[4]) at its full size on this GPU: 10 000
     synthetic ligands (U[10,100] atoms, U[0,30] torsions) against the C4
     receptor (126^3 maps), `runs` LGA runs each, docked + clustered through
@@ -733,7 +733,7 @@ def c5_measure(torch, local, n_ligands=10_000, runs=10, method="baseline", batch
     dg = dev.grid_build(sites, fields, grid)
     s = LgaSettings(partition=64)
     ligs = [c5_ligand(j, sites) for j in range(n_ligands)]
-    warm = sc.screen(dev, dg, lambda j: ligs[j], 2 * batch, runs, s, METHODS[method], batch=batch)
+    warm = sc.screen(dev, dg, lambda j: ligs[j], min(2 * batch, n_ligands), runs, s, METHODS[method], batch=batch)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rows, clusters = sc.screen(dev, dg, lambda j: ligs[j], n_ligands, runs, s, METHODS[method], batch=batch)

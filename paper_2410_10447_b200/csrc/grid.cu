@@ -22,6 +22,10 @@
 // driver's bookkeeping kernels (lga_device.cuh, dock.cu).
 #include <cuda_runtime.h>
 
+#ifndef MDR_GRID_NO_GATHER
+#define MDR_GRID_NO_GATHER 0
+#endif
+
 #include "dock_launch.h"
 #include "lga_device.cuh"
 #include "mdr_device.cuh"
@@ -163,9 +167,20 @@ __device__ __forceinline__ float grid_atom(const GridView& G, int type, float w,
   const float aq = fabsf(q);
   const long long co[8] = {0, 1, nx, nx + 1, nxy, nxy + 1, nxy + nx, nxy + nx + 1};
   float c[8];
+#if MDR_GRID_NO_GATHER
+  // timing probe only (wrong results): the map values replaced by a function
+  // of the corner offset, to bound what any map layout / staging could gain
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = fmaf(w, (float)(o & 7) * 0.01f, q * 0.001f * (float)k + aq * 0.0001f);
+  (void)mt;
+  (void)me;
+  (void)md;
+  (void)co;
+#else
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     c[k] = fmaf(w, __ldg(mt + co[k]), fmaf(q, __ldg(me + co[k]), aq * __ldg(md + co[k])));
+#endif
   // x pass (k = dz*4 + dy*2 + dx), y pass, z pass
   float gx[4], vx[4];
 #pragma unroll
