@@ -242,6 +242,15 @@ void pick_search_items(int na, int ns, int force_len, int force_group, int& n_ch
   n_chunks = 1;
   chunk_len = ns;
   group = 1;
+  if (force_len > 0) {  // timing / test override (MDR_LS_CHUNK_LEN, MDR_LS_GROUP): any length, 1-3 atoms per item
+    const int n = (ns + force_len - 1) / force_len;
+    if (n > 1 && na * n <= kMaxChunkItemsForced && na * n > 32) {
+      n_chunks = n;
+      chunk_len = force_len;
+      group = force_group >= 1 && force_group <= 3 ? force_group : 1;
+    }
+    return;
+  }
   long best = (long)((na + 31) / 32) * ns;
   for (int G : {1, 3}) {
     if (force_group > 0 && G != force_group) continue;
@@ -250,15 +259,13 @@ void pick_search_items(int na, int ns, int force_len, int force_group, int& n_ch
       if (na * n > kMaxChunkItems || na * n <= 32) continue;
       const int items = (na + G - 1) / G * n;
       const long cost = (long)((items + 63) / 64) * G * len;
-      if (force_len > 0 ? len == force_len : cost < best) {
+      if (cost < best) {
         best = cost;
         n_chunks = n;
         chunk_len = len;
         group = G;
-        if (force_len > 0) break;
       }
     }
-    if (force_len > 0 && n_chunks > 1) break;
   }
 }
 

@@ -17,7 +17,9 @@ constexpr int kMaxSites = 2048;    // per-CTA shared-memory copy
 constexpr int kMaxAtoms = 4096;
 constexpr int kWindow = 16;        // local_search convergence window, docking.cpp:314
 constexpr int kMaxExactAtoms = 1024;
-constexpr int kMaxChunkItems = 256;   // atoms x site chunks staged per warp (32 B each)  // exact-torsion mode stages one float4 torque per atom per warp
+constexpr int kMaxChunkItems = 256;        // policy limit (pick_chunks / pick_search_items)
+constexpr int kMaxChunkItemsForced = 512;  // with a pinned chunk length (timing / tests)
+//    // atoms x site chunks staged per warp (32 B each)  // exact-torsion mode stages one float4 torque per atom per warp
 
 // One receptor site with the two pair-loop constants precomputed on the host
 // in the reference's evaluation order (docking.cpp:114-116):
