@@ -281,7 +281,7 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   // the warp-per-pose kernels (score, init, offspring, one-warp search,
   // polish) spread chunk items over 32 lanes; the LGA's multi-warp search
   // over the 64 lanes of its warp pair (ls_multi.cu or the legacy kernel)
-  const bool multi = c->ls_pair && c->ls_warps != 1 && !c->exact && c->wpb <= 8 && c->cta_warps == 0;
+  const bool multi = c->ls_pair && c->ls_warps != 1 && !c->exact && c->wpb <= 7 && c->cta_warps == 0;
   const int search_lanes = multi ? 64 : 32;
   L.ls_group = 1;
   if (c->pair == MDR_PAIR_FP64_FAST && c->chunking) {

@@ -569,7 +569,7 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
   const int run = item / D.L, r = item % D.L;
   if (!D.active[run]) return;
   WarpCtx w = warp_region(smem + ligand_smem_bytes(L), pose, L);
-  w.ws.bar = 1 + pose;
+  w.ws.bar = 1 + 2 * pose;  // B1; B2 = bar + 1
 #if MDR_PHASE_PROF
   // leader: phases 0-6 (+ [7] evaluations); helper: 8-10 (own slots)
   if (lane == 0) {
@@ -583,12 +583,13 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
     // the helper keeps its own last stamp in slot 14
     long long* pf = w.ws.prof;
     for (;;) {
-      pair_bar(w.ws.bar);
+      nbar_sync(w.ws.bar, 64);
       if (lane == 0) { const long long t = clock64(); pf[8] += t - pf[14]; pf[14] = t; }
       if (*w.ws.ctl == 0) break;
       fast_sums_items(S, w.ws, 32 + lane, 64);
       if (lane == 0) { const long long t = clock64(); pf[9] += t - pf[14]; pf[14] = t; }
-      pair_bar(w.ws.bar);
+      __syncwarp();
+      nbar_arrive(w.ws.bar + 1, 64);
       if (lane == 0) { const long long t = clock64(); pf[10] += t - pf[14]; pf[14] = t; }
     }
     if (lane == 0)
@@ -607,7 +608,8 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
   const LsResult res = local_search_warp<METHOD, MDR_PAIR_FP64_FAST, false, 2>(S, start, D.ls_iters, D.tol,
                                                                               D.partition, D.half_mode != 0, w);
   if (lane == 0) *w.ws.ctl = 0;
-  pair_bar(w.ws.bar);  // release the helper
+  __syncwarp();
+  nbar_arrive(w.ws.bar, 64);  // release the helper
 #if MDR_PHASE_PROF
   if (lane == 0) {
     for (int k = 0; k <= 6; ++k) atomicAdd(&g_phase[k], (unsigned long long)w.ws.prof[k]);
@@ -1000,15 +1002,15 @@ cudaError_t launch_local_search(const LigandView& L, const double* starts, int n
   return cudaGetLastError();
 }
 
-// Warp-pair Lamarckian search (lga_ls_pair_kernel): FP64-fast chunked
-// ligands with more than one wave of chunk items, at most 8 searches per CTA
-// (named barriers 1..8).
+// Legacy warp-pair Lamarckian search (lga_ls_pair_kernel): FP64-fast chunked
+// ligands the two-warp kernel does not take (n_atoms or dim > 32), at most 7
+// searches per CTA (two named barriers each, ids 1..14).
 #ifndef MDR_LS_PAIR
 #define MDR_LS_PAIR 1
 #endif
 static bool use_ls_pair(const LigandView& L, int pair, int wpb, int cta_warps) {
   return MDR_LS_PAIR && L.ls_pair && L.ls_warps != 1 && cta_warps == 0 && pair == MDR_PAIR_FP64_FAST &&
-         L.ls_n_chunks > 1 && !L.exact_torsion && L.n_atoms * L.ls_n_chunks > 32 && wpb <= 8;
+         L.ls_n_chunks > 1 && !L.exact_torsion && L.n_atoms * L.ls_n_chunks > 32 && wpb <= 7;  // 2 barriers per search
 }
 static cudaError_t prep_ls_pair(int method, size_t smem) {
   switch (method) {

@@ -1,7 +1,10 @@
 """Small end-to-end pass over every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): analytic score / LS / LGA (all pair
-modes, all reduction methods), grid build / score / LS / LGA / screen,
-clustering, reductions and the half/mma units."""
+modes, all reduction methods), the LGA's two-warp persistent search and
+polish (named-barrier arrive/sync protocol, padded site chunks) and the
+other search configurations, grid build / score / LS / LGA / screen,
+clustering, reductions (incl. the batched tcgen05 contraction) and the
+half/mma units."""
 import json, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -42,4 +45,19 @@ ligs, prms = zip(*[c5_ligand(j, sites) for j in range(3)])
 dev.grid_screen_batch(dg, list(ligs), list(prms), 2, BASELINE,
                       LgaSettings(generations=1, population_size=6, ls_max_iters=6, partition=64),
                       np.arange(6, dtype=np.uint64), 2.0)
+# chunked small ligand: the two-warp persistent search (ls_multi.cu), its
+# polish, and the one-warp / legacy-pair configurations
+from paper_2410_10447_b200.workloads import c3  # noqa: E402
+
+for warps in (2, 1, 0):
+    d = Device(0, pair=PAIR_FP64_FAST)
+    assert d.lib.mdr_ctx_set_ls_warps(d.ctx, warps) == 0
+    for m, acc in ((BASELINE, SINGLE), (TCU_SPLIT, SINGLE)):
+        d.lga_run_batch(c3(), m, acc, LgaSettings(generations=2, ls_max_iters=20), [11, 12, 13])
+    d.close()
+# TcuSplit batches routed to tcgen05 (float4 and Partial7 forms, ragged tail)
+n_red = 148 * 32 + 5
+assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, 32, n_red) == 1
+dev.reduce4_batch(np.random.default_rng(2).uniform(-1, 1, (n_red, 32, 4)).astype(np.float32), SINGLE, TCU_SPLIT)
+dev.reduce7_batch(np.random.default_rng(3).uniform(-1, 1, (n_red, 32, 7)).astype(np.float32), TCU_SPLIT, SINGLE)
 print("sanitize driver done")
