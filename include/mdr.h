@@ -211,6 +211,10 @@ int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatch
  * against this host's glibc over n counter-generated inputs.  mismatches[8]:
  * cr sin, cr cos, cr log, cr cos2pi, libdevice sin, cos, log, cos2pi. */
 int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches);
+/* The raw values behind mdr_selftest_crmath for inputs i0 .. i0+n-1:
+ * out[8 i + 0..3] = correctly rounded sin a, cos a, log u1, cos z (the
+ * grid-mode and Box-Muller math), out[8 i + 4..7] = libdevice's. */
+int mdr_crmath_values(mdr_ctx* ctx, int64_t i0, int n, double* out);
 
 /* C2 microbench (no reference counterpart; cli.cpp:195-266 is its CPU
  * analogue): kernel k in [0, mdr_reduce_bench_kernels()) reduces float4 per

@@ -20,6 +20,7 @@
 #include <string.h>
 
 #include "mdr.h"
+#include "crmath.h"
 
 #define ORC_PI 3.14159265358979323846
 
@@ -56,6 +57,12 @@ static double orc_normal(orc_rng* r) { /* rng.cpp:47-52, exactly two draws */
   const double u1 = (double)((orc_u64(r) >> 11) + 1) * 0x1p-53;
   const double u2 = orc_unit(r);
   return sqrt(-2.0 * log(u1)) * cos(2.0 * ORC_PI * u2);
+}
+/* The same draw with correctly rounded log / cos (grid mode, crmath.h). */
+static double orc_normal_cr(orc_rng* r) {
+  const double u1 = (double)((orc_u64(r) >> 11) + 1) * 0x1p-53;
+  const double u2 = orc_unit(r);
+  return sqrt(-2.0 * cr_log(u1)) * cr_cos(2.0 * ORC_PI * u2);
 }
 static uint64_t orc_index(orc_rng* r, uint64_t n) { return n == 0 ? 0 : orc_u64(r) % n; }
 
@@ -348,9 +355,22 @@ typedef struct {
   v3* tors_world; /* n_rot */
 } frame_t;
 
-/* build_frame docking.cpp:78-91 */
-static void build_frame(const mdr_instance* in, const double* g, frame_t* f) {
-  const m3 a = rz(g[3]), b = ry(g[4]), c = rz(g[5]);
+static m3 rz_cr(double a) { /* rz with correctly rounded trig (grid mode) */
+  double s, c;
+  cr_sincos(a, &s, &c);
+  m3 r = {{{c, -s, 0.0}, {s, c, 0.0}, {0.0, 0.0, 1.0}}};
+  return r;
+}
+static m3 ry_cr(double a) {
+  double s, c;
+  cr_sincos(a, &s, &c);
+  m3 r = {{{c, 0.0, s}, {0.0, 1.0, 0.0}, {-s, 0.0, c}}};
+  return r;
+}
+
+/* build_frame docking.cpp:78-91; cr: correctly rounded trig (grid mode) */
+static void build_frame_x(const mdr_instance* in, const double* g, frame_t* f, int cr) {
+  const m3 a = cr ? rz_cr(g[3]) : rz(g[3]), b = cr ? ry_cr(g[4]) : ry(g[4]), c = cr ? rz_cr(g[5]) : rz(g[5]);
   const m3 ab = mm3(&a, &b);
   f->R = mm3(&ab, &c);
   v3 ez = {{0.0, 0.0, 1.0}}, ey = {{0.0, 1.0, 0.0}};
@@ -359,6 +379,7 @@ static void build_frame(const mdr_instance* in, const double* g, frame_t* f) {
   f->ax_alpha = mv3(&ab, ez);
   for (int k = 0; k < in->n_rot; ++k) f->tors_world[k] = mv3(&f->R, orc_torsion_axis(k));
 }
+static void build_frame(const mdr_instance* in, const double* g, frame_t* f) { build_frame_x(in, g, f, 0); }
 
 typedef struct {
   double e;
@@ -631,7 +652,7 @@ int orc_lga_max_records(const mdr_lga_settings* s) {
 /* lga_run docking.cpp:392-517 */
 static int lga_core(orc_scorefn fn, const void* sctx, const mdr_instance* in, const mdr_lga_settings* s,
                     uint64_t seed, double* best_e, double* best_g, int64_t* evals_out, int32_t* conv,
-                    int32_t* n_records, mdr_ls_record* records, int max_records) {
+                    int32_t* n_records, mdr_ls_record* records, int max_records, int cr) {
   const int dim = 6 + in->n_rot, P = s->population_size;
   orc_rng r = orc_rng_make(seed, "lga");
   double* pop = (double*)malloc(sizeof(double) * (size_t)(P * dim));
@@ -691,7 +712,7 @@ static int lga_core(orc_scorefn fn, const void* sctx, const mdr_instance* in, co
           const double lam = orc_unit(&r);
           ch[d] = lam * pop[a * dim + d] + (1.0 - lam) * pop[b * dim + d];
         }
-        for (int d = 0; d < dim; ++d) ch[d] = ch[d] + s->mutation_sigma * orc_normal(&r);
+        for (int d = 0; d < dim; ++d) ch[d] = ch[d] + s->mutation_sigma * (cr ? orc_normal_cr(&r) : orc_normal(&r));
         normalize_angles(ch, dim);
         rc = fn(sctx, ch, &e, gr);
         if (rc) goto done;
@@ -765,7 +786,7 @@ int orc_lga_run(const mdr_instance* in, int method, int accum, const mdr_lga_set
   if (in->n_rot > 58) return MDR_ERR_SIZE;
   const analytic_sctx a = {in, method, accum, s->partition};
   const int rc = lga_core(analytic_score, &a, in, s, seed, best_e, best_g, evals_out, conv, n_records, records,
-                          max_records);
+                          max_records, 0);
   if (st) {
     mdr_sync_stats one;
     score_stats(method, accum, s->partition, &one);
@@ -890,7 +911,7 @@ int orc_grid_score(const mdr_instance* in, const mdr_grid* G, const mdr_ligand_p
   frame_t f;
   v3 tw[64];
   f.tors_world = tw;
-  build_frame(in, g, &f);
+  build_frame_x(in, g, &f, 1);  /* grid mode: correctly rounded trig (crmath.h) */
   const int na = in->n_atoms;
   v3* r = (v3*)malloc(sizeof(v3) * (size_t)na);
   v3* F = (v3*)calloc((size_t)na, sizeof(v3));
@@ -904,7 +925,9 @@ int orc_grid_score(const mdr_instance* in, const mdr_grid* G, const mdr_ligand_p
     const int k = in->atom_torsion[i];
     if (k >= 0) {
       const v3 ax = orc_torsion_axis(k);
-      const double ang = g[6 + k], c = cos(ang), s = sin(ang);
+      const double ang = g[6 + k];
+      double c, s;
+      cr_sincos(ang, &s, &c);
       local = add3(add3(scl3(c, local), scl3(s, cross3(ax, local))), scl3((1.0 - c) * dot3(ax, local), ax));
     }
     r[i] = mv3(&f.R, local);
@@ -977,7 +1000,7 @@ int orc_grid_lga_run(const mdr_instance* in, const mdr_grid* G, const mdr_ligand
   if (in->n_rot > 58) return MDR_ERR_SIZE;
   const grid_sctx c = {in, G, P};
   return lga_core(grid_score_fn, &c, in, s, seed, best_e, best_g, evals_out, conv, n_records, records,
-                  max_records);
+                  max_records, 1);
 }
 
 /* ======================================================== RMSD clustering
@@ -1063,4 +1086,20 @@ int orc_cluster_poses(const mdr_instance* in, const double* genos, const double*
   *n_clusters = nc;
   free(xyz); free(order); free(seeds);
   return rc;
+}
+
+/* Test support: crmath.h's correctly rounded sin / cos / log on the inputs
+ * of the device's crmath probe (mdr_crmath_values): input i is a = -pi + 2 pi
+ * u(4i+1), u1 = ((u(4i+2) >> 11) + 1) 2^-53, z = 2 pi u(4i+3), with u(n) the
+ * key-0 RngStream draw n.  out[4 i + 0..3] = sin a, cos a, log u1, cos z. */
+void orc_cr_values(int64_t i0, int n, double* out) {
+  for (int t = 0; t < n; ++t) {
+    const uint64_t i = (uint64_t)(i0 + t);
+    const double a = -ORC_PI + 2.0 * ORC_PI * ((double)(orc_mix64((4 * i + 1) * 0x9e3779b97f4a7c15ull) >> 11) * 0x1p-53);
+    const double u1 = (double)((orc_mix64((4 * i + 2) * 0x9e3779b97f4a7c15ull) >> 11) + 1) * 0x1p-53;
+    const double z = 2.0 * ORC_PI * ((double)(orc_mix64((4 * i + 3) * 0x9e3779b97f4a7c15ull) >> 11) * 0x1p-53);
+    cr_sincos(a, &out[4 * t], &out[4 * t + 1]);
+    out[4 * t + 2] = cr_log(u1);
+    out[4 * t + 3] = cr_cos(z);
+  }
 }

@@ -306,3 +306,38 @@ def lga_runs_parallel(kind, inst, method, accum, settings: LgaSettings, seeds, p
     jobs = [(kind, inst, method, accum, settings, int(s)) for s in seeds]
     with mp.get_context("spawn").Pool(procs) as pool:
         return pool.map(_lga_job, jobs)
+
+
+_GRID_JOB = {}  # (inst, grid, params, settings) shared with forked workers
+
+
+def _grid_lga_job(seed):
+    inst, grid, params, settings = _GRID_JOB["case"]
+    r = Oracle("port").grid_lga_run(inst, grid, params, settings, int(seed))
+    return r["best_energy"], r["evaluations"], r["converged"], np.asarray(r["best_genotype"]).copy()
+
+
+def grid_lga_runs_parallel(inst, grid, params, settings: LgaSettings, seeds, procs=None):
+    """Test infrastructure: oracle grid-mode LGA runs (orc_grid_lga_run), one
+    per seed, on `fork`ed worker processes that inherit the maps (tens of MB)
+    instead of receiving them pickled; the workers only call the C oracle.
+    Returns (best_energy, evaluations, converged, best_genotype) per seed."""
+    import multiprocessing as mp
+
+    _GRID_JOB["case"] = (inst, grid, params, settings)
+    procs = procs or min(len(seeds), os.cpu_count() or 1)
+    try:
+        with mp.get_context("fork").Pool(procs) as pool:
+            return pool.map(_grid_lga_job, [int(s) for s in seeds])
+    finally:
+        _GRID_JOB.clear()
+
+
+def cr_values(i0: int, n: int) -> np.ndarray:
+    """crmath.h's correctly rounded sin a, cos a, log u1, cos z on the
+    device crmath probe's inputs (see orc_cr_values); shape (n, 4)."""
+    lib = Oracle("port").lib
+    out = np.zeros((n, 4))
+    lib.orc_cr_values.argtypes = [C.c_int64, C.c_int, C.c_void_p]
+    lib.orc_cr_values(i0, n, out.ctypes.data)
+    return out

@@ -72,6 +72,7 @@ _SIGS = {
     "mdr_selftest_dsqrt": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_sincos": (I, [P, U64, C.c_int64, P]),
     "mdr_selftest_crmath": (I, [P, C.c_int64, P]),
+    "mdr_crmath_values": (I, [P, C.c_int64, I, P]),
     "mdr_reduce_bench_dev": (I, [P, I, I, P, I, I, P]),
     "mdr_fill_uniform_dev": (I, [P, U64, C.c_char_p, C.c_int64, P]),
     "mdr_reduce_bench_chain_cycles_dev": (I, [P, I, I, P, I, I, P, P]),

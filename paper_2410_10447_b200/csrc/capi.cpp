@@ -679,6 +679,18 @@ int mdr_selftest_ddiv(mdr_ctx* ctx, uint64_t seed, int64_t n, uint64_t* mismatch
 
 // C2 microbench: one block-level float4 reduce-and-broadcast per thread
 // block (see bench_reduce.cu for the kernel roster).
+int mdr_crmath_values(mdr_ctx* ctx, int64_t i0, int n, double* out) {
+  if (!ctx || n < 0 || (n && !out)) return fail(ctx, MDR_ERR_INVALID, "bad argument");
+  if (n == 0) return MDR_OK;
+  DevBuf<double> d;
+  CK(d.alloc((size_t)8 * n, S(ctx)));
+  CK(launch_crmath_probe((long long)i0, n, d.p, S(ctx)));
+  ctx->launches++;
+  CK(cudaMemcpyAsync(out, d.p, sizeof(double) * 8 * n, cudaMemcpyDeviceToHost, S(ctx)));
+  CK(cudaStreamSynchronize(S(ctx)));
+  return MDR_OK;
+}
+
 int mdr_selftest_crmath(mdr_ctx* ctx, int64_t n, uint64_t* mismatches) {
   if (!ctx || n < 0 || !mismatches) return fail(ctx, MDR_ERR_INVALID, "bad argument");
   std::memset(mismatches, 0, sizeof(uint64_t) * 8);
@@ -919,12 +931,19 @@ struct InstanceGuard {
   ~InstanceGuard() { mdr_instance_free(ctx, di); }
 };
 
+// Grid kernels run the strict FP64 path (the oracle's arithmetic and order,
+// grid.cu grid_eval_strict) when the context's pair precision is
+// MDR_PAIR_FP64, the FP32 path with the requested reduction otherwise.
+static int grid_method(const mdr_ctx* ctx, int method) {
+  return ctx->pair == MDR_PAIR_FP64 ? kGridStrictMethod : method;
+}
+
 // Grid mode runs one CTA of `partition` threads per pose: thread d owns
 // genotype dimension d, so the block must cover the genotype.
 static int check_grid_block(mdr_ctx* ctx, const mdr_dev_instance* di, int partition) {
   if (partition < 6 + di->n_rot)
     return fail(ctx, MDR_ERR_BLOCK_SIZE, "grid mode needs partition >= 6 + n_rot (one thread per dimension)");
-  if (grid_smem_for(di->view, di->flex, partition) > 227 * 1024)
+  if (grid_smem_for(di->view, di->flex, partition, grid_method(ctx, MDR_METHOD_BASELINE)) > 227 * 1024)
     return fail(ctx, MDR_ERR_SIZE, "grid-mode ligand does not fit in shared memory");
   return MDR_OK;
 }
@@ -941,7 +960,8 @@ int mdr_score_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double* g, int
   if (di->grid) {
     if (int rc = check_grid_block(ctx, di, partition)) return rc;
     if (n <= 0) return MDR_OK;
-    CK(launch_grid_score(di->view, di->gview, di->flex, g, n, method, partition, e, grad, tq, ctx->stream));
+    CK(launch_grid_score(di->view, di->gview, di->flex, g, n, grid_method(ctx, method), partition, e, grad, tq,
+                         ctx->stream));
     ctx->launches++;
     return MDR_OK;
   }
@@ -1042,7 +1062,8 @@ int mdr_local_search_dev(mdr_ctx* ctx, const mdr_dev_instance* di, const double*
   if (di->grid) {
     if (int rc = check_grid_block(ctx, di, partition)) return rc;
     if (n <= 0) return MDR_OK;
-    CK(launch_grid_local_search(di->view, di->gview, di->flex, starts, n, max_iters, tol, method, partition, og, oe,
+    CK(launch_grid_local_search(di->view, di->gview, di->flex, starts, n, max_iters, tol, grid_method(ctx, method),
+                                partition, og, oe,
                                 oit, ocv, status, ctx->stream));
     ctx->launches++;
     return MDR_OK;
@@ -1134,6 +1155,7 @@ struct mdr_lga_batch {
   GridLigands GL{};    // device tables (one ligand, or a screen batch)
   void* gl_block = nullptr;
   size_t gsm = 0;      // dynamic shared memory of the grid kernels
+  int gmethod = 0;     // grid kernels' method (kGridStrictMethod: strict FP64 path)
 };
 
 static uint64_t mix64_host(uint64_t z) {
@@ -1242,7 +1264,7 @@ static void lga_batch_release(mdr_lga_batch* b) {
 // profiling replay with events).
 static cudaError_t lga_batch_enqueue(mdr_lga_batch* b, cudaStream_t s, int wpb, int* launches,
                                      cudaEvent_t* ev = nullptr) {
-  if (b->grid) return launch_grid_lga(b->GL, b->gsm, b->G, b->D, b->method, b->D.partition, s, launches, ev);
+  if (b->grid) return launch_grid_lga(b->GL, b->gsm, b->G, b->D, b->gmethod, b->D.partition, s, launches, ev);
   return launch_lga(b->L, b->D, b->method, b->pair, s, wpb, b->cta_warps, launches, ev);
 }
 
@@ -1270,8 +1292,9 @@ mdr_lga_batch* mdr_lga_batch_create(mdr_ctx* ctx, const mdr_dev_instance* di, in
     b->GL.L = static_cast<const LigandView*>(b->gl_block);
     b->GL.F = reinterpret_cast<const FlexView*>(static_cast<char*>(b->gl_block) + 256);
     b->GL.run_lig = nullptr;
-    b->gsm = grid_smem_for(di->view, di->flex, s->partition);
-    if (e == cudaSuccess) e = prepare_grid_lga(b->gsm, method);
+    b->gmethod = grid_method(ctx, method);
+    b->gsm = grid_smem_for(di->view, di->flex, s->partition, b->gmethod);
+    if (e == cudaSuccess) e = prepare_grid_lga(b->gsm, b->gmethod);
   } else {
     e = prepare_lga(b->L, method, b->pair, ctx->wpb, b->cta_warps);
   }
@@ -1523,7 +1546,7 @@ void mdr_grid_free(mdr_ctx* ctx, mdr_dev_grid* d) {
 // {radius, sqrt(epsilon), q, k_e q} and the torsion-group CSR.
 static int prep_flex(mdr_ctx* ctx, int na, int nr, const int* tors, const mdr_ligand_params* p, int n_types,
                      std::vector<int>& type, std::vector<float4>& chem, std::vector<int>& off,
-                     std::vector<int>& members) {
+                     std::vector<int>& members, std::vector<double4>* chem64 = nullptr) {
   if (!p || !p->atom_type || !p->atom_charge || !p->atom_radius || !p->atom_epsilon)
     return fail(ctx, MDR_ERR_INVALID, "null ligand parameters");
   type.assign(na, 0);
@@ -1536,6 +1559,10 @@ static int prep_flex(mdr_ctx* ctx, int na, int nr, const int* tors, const mdr_li
     type[i] = p->atom_type[i];
     chem[i] = make_float4((float)p->atom_radius[i], (float)std::sqrt(p->atom_epsilon[i]), (float)p->atom_charge[i],
                           (float)(p->elec_scale * p->atom_charge[i]));
+    if (chem64) {
+      if (i == 0) chem64->assign(na, double4{});
+      (*chem64)[i] = make_double4(p->atom_radius[i], p->atom_epsilon[i], p->atom_charge[i], 0.0);
+    }
   }
   off.assign(nr + 1, 0);
   members.clear();
@@ -1557,12 +1584,14 @@ int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid
   const int na = di->n_atoms, nr = di->n_rot;
   std::vector<int> tors(na), type, off, members;
   std::vector<float4> chem;
+  std::vector<double4> chem64;
   CK(cudaMemcpy(tors.data(), di->view.tors, sizeof(int) * na, cudaMemcpyDeviceToHost));
-  if (int rc = prep_flex(ctx, na, nr, tors.data(), p, g->view.n_types, type, chem, off, members)) return rc;
+  if (int rc = prep_flex(ctx, na, nr, tors.data(), p, g->view.n_types, type, chem, off, members, &chem64)) return rc;
   const int nta = (int)members.size();
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t o_type = 0, o_chem = al(sizeof(int) * na), o_off = o_chem + al(sizeof(float4) * na),
-               o_mem = o_off + al(sizeof(int) * (nr + 1)), total = o_mem + al(sizeof(int) * std::max(nta, 1));
+               o_mem = o_off + al(sizeof(int) * (nr + 1)), o_c64 = o_mem + al(sizeof(int) * std::max(nta, 1)),
+               total = o_c64 + al(sizeof(double4) * std::max(na, 1));
   if (di->flex_block) {
     CK(cudaStreamSynchronize(ctx->stream));
     cudaFree(di->flex_block);
@@ -1574,7 +1603,10 @@ int mdr_instance_set_grid(mdr_ctx* ctx, mdr_dev_instance* di, const mdr_dev_grid
   CK(cudaMemcpy(b + o_chem, chem.data(), sizeof(float4) * na, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(b + o_off, off.data(), sizeof(int) * (nr + 1), cudaMemcpyHostToDevice));
   if (nta) CK(cudaMemcpy(b + o_mem, members.data(), sizeof(int) * nta, cudaMemcpyHostToDevice));
+  if (na) CK(cudaMemcpy(b + o_c64, chem64.data(), sizeof(double4) * na, cudaMemcpyHostToDevice));
   FlexView& F = di->flex;
+  F.chem64 = reinterpret_cast<const double4*>(b + o_c64);
+  F.elec_scale = p->elec_scale;
   F.type = reinterpret_cast<const int*>(b + o_type);
   F.chem = reinterpret_cast<const float4*>(b + o_chem);
   F.grp_off = reinterpret_cast<const int*>(b + o_off);
@@ -1726,7 +1758,7 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instanc
     if (int rc = prep_flex(ctx, L.na, L.nr, in->atom_torsion, &params[j], g->view.n_types, type, chem, off, members))
       return rc;
     L.nta = (int)members.size();
-    const size_t sm = grid_smem_for(L.na, L.nr, L.nta, T);
+    const size_t sm = grid_smem_for(L.na, L.nr, L.nta, T);  // screening: the FP32 grid path
     if (sm > 227 * 1024) return fail(ctx, MDR_ERR_SIZE, "grid-mode ligand does not fit in shared memory");
     max_smem = std::max(max_smem, sm);
     max_dim = std::max(max_dim, 6 + L.nr);
@@ -1798,6 +1830,7 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instanc
   b->GL.F = reinterpret_cast<const FlexView*>(base + o_flex);
   b->GL.run_lig = reinterpret_cast<const int*>(base + o_rl);
   b->gsm = max_smem;
+  b->gmethod = method;  // screening runs the FP32 grid path
   CK(prepare_grid_lga(b->gsm, method));
   CK(cudaMemcpyAsync(b->seeds, seeds, sizeof(uint64_t) * R, cudaMemcpyHostToDevice, S(ctx)));
   int launches = 0;

@@ -26,7 +26,9 @@ cudaError_t launch_lga_init_finalize(const LgaDev& D, cudaStream_t s);
 cudaError_t launch_lga_gen_finalize(const LgaDev& D, int gen, cudaStream_t s);
 
 // grid.cu (grid-map scoring mode, CTA of `threads` per pose)
-size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads);
+size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads, int method);
+// grid kernels' method code of the strict FP64 path (grid.cu kGridStrict)
+constexpr int kGridStrictMethod = 3;
 cudaError_t launch_grid_score(const LigandView& L, const GridView& G, const FlexView& F, const double* genos, int n,
                               int method, int threads, float* energy, float* grad, float* torque, cudaStream_t s);
 cudaError_t launch_grid_local_search(const LigandView& L, const GridView& G, const FlexView& F, const double* starts,

@@ -29,6 +29,7 @@
 #include "dock_launch.h"
 #include "lga_device.cuh"
 #include "mdr_device.cuh"
+#include "crmath.cuh"
 
 // Phase A trig in FP32: C4 43.7 -> 55.3 M evals/s (the other threads wait
 // at S1 for it), device-vs-oracle error 1.0e-6 -> 1.4e-6 (energy), 1.6e-6 ->
@@ -43,6 +44,13 @@
 namespace mdr {
 
 // ------------------------------------------------------------ smem layout
+__host__ __device__ inline size_t al16_(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Method code of the strict FP64 grid path (the context's pair precision
+// MDR_PAIR_FP64): the oracle's double arithmetic in the oracle's order,
+// correctly rounded trig (csrc/crmath.cuh, oracle/crmath.h).
+constexpr int kGridStrict = 3;
+
 struct GridSmem {
   double4* atoms;   // na: local x, y, z, weight
   int* tors;        // na
@@ -61,7 +69,21 @@ struct GridSmem {
   double* best;     // dim
   unsigned char* scratch;  // W x kWarpScratchBytes (MMA staging)
   int na, nr, nta, C, W;
+  // strict FP64 mode (METHOD == kGridStrict) only:
+  double4* xr;          // na: lever arm r_i = R local_i (x, y, z)
+  double4* xf;          // na: grid force F_i (x, y, z) and energy term (w)
+  double4* xfi;         // na: intramolecular force Fi_i
+  double* xep;          // na (na - 1) / 2: pair energies, row i holds pairs (i, j > i)
+  double* xtot;         // 8: energy, sum F (3), sum r x F (3)
+  const double4* chem64;  // na: radius, epsilon, charge (double, as the oracle)
+  double elec_scale;
 };
+
+// Strict FP64 grid mode: the extra shared memory (after the MMA scratch).
+__host__ __device__ inline size_t grid_strict_bytes(int na) {
+  return al16_(sizeof(double4) * (size_t)na) * 3 + al16_(sizeof(double) * ((size_t)na * (na - 1) / 2 + 1)) +
+         al16_(sizeof(double) * 8);
+}
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
@@ -91,7 +113,7 @@ __host__ __device__ inline size_t grid_smem_bytes(int na, int nr, int nta, int T
   return b;
 }
 
-__device__ GridSmem grid_load(const LigandView& L, const FlexView& F, unsigned char* base) {
+__device__ GridSmem grid_load(const LigandView& L, const FlexView& F, unsigned char* base, bool strict = false) {
   GridSmem S;
   S.na = L.n_atoms;
   S.nr = L.n_rot;
@@ -122,6 +144,18 @@ __device__ GridSmem grid_load(const LigandView& L, const FlexView& F, unsigned c
   S.g = reinterpret_cast<double*>(take(sizeof(double) * dim));
   S.best = reinterpret_cast<double*>(take(sizeof(double) * dim));
   S.scratch = p;
+  S.xr = S.xf = S.xfi = nullptr;
+  S.xep = S.xtot = nullptr;
+  S.chem64 = F.chem64;
+  S.elec_scale = F.elec_scale;
+  if (strict) {
+    p += (size_t)kWarpScratchBytes * S.W;
+    S.xr = reinterpret_cast<double4*>(take(sizeof(double4) * na));
+    S.xf = reinterpret_cast<double4*>(take(sizeof(double4) * na));
+    S.xfi = reinterpret_cast<double4*>(take(sizeof(double4) * na));
+    S.xep = reinterpret_cast<double*>(take(sizeof(double) * ((size_t)na * (na - 1) / 2 + 1)));
+    S.xtot = reinterpret_cast<double*>(take(sizeof(double) * 8));
+  }
   for (int i = threadIdx.x; i < na; i += blockDim.x) {
     S.atoms[i] = L.atoms[i];
     S.tors[i] = L.tors[i];
@@ -251,9 +285,235 @@ struct GridEval {
   float e;   // total energy (all threads)
   float gd;  // gradient component threadIdx.x (threads < dim)
 };
+struct GridEvalD {  // the strict FP64 path's (double energy and gradient, as the oracle)
+  double e;
+  double gd;
+};
+template <int METHOD>
+struct GridEvalT {
+  using type = GridEval;
+};
+template <>
+struct GridEvalT<kGridStrict> {
+  using type = GridEvalD;
+};
+
+// Trilinear sample of the combined map in double, operation for operation
+// the oracle's grid_sample (oracle/mdr_oracle.c): IEEE divisions by the
+// spacing, no contraction (the library is built with --fmad=false).
+__device__ __forceinline__ double grid_sample_f64(const GridView& G, int type, double w, double q, const double p[3],
+                                                  double dvdp[3], double off[3]) {
+  const int n[3] = {G.nx, G.ny, G.nz};
+  const double org[3] = {G.ox, G.oy, G.oz};
+  int i0[3];
+  double f[3];
+  bool inside[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double gc = (p[a] - org[a]) / G.h;
+    double gcc = gc < 0.0 ? 0.0 : gc;
+    gcc = gcc > (double)(n[a] - 1) ? (double)(n[a] - 1) : gcc;
+    int i = (int)floor(gcc);
+    if (i > n[a] - 2) i = n[a] - 2;
+    i0[a] = i;
+    f[a] = gcc - i;
+    inside[a] = gc >= 0.0 && gc <= (double)(n[a] - 1);
+    off[a] = G.h * (gc - gcc);
+  }
+  const size_t stride = (size_t)G.stride;
+  const float* mt = G.maps + (size_t)type * stride;
+  const float* me = G.maps + (size_t)G.n_types * stride;
+  const float* md = me + stride;
+  const double aq = fabs(q);
+  double c[2][2][2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const size_t o = ((size_t)(i0[2] + dz) * G.ny + (i0[1] + dy)) * G.nx + (i0[0] + dx);
+        c[dz][dy][dx] = w * (double)__ldg(mt + o) + q * (double)__ldg(me + o) + aq * (double)__ldg(md + o);
+      }
+  double vx[2][2], gx[2][2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      gx[dz][dy] = c[dz][dy][1] - c[dz][dy][0];
+      vx[dz][dy] = c[dz][dy][0] + f[0] * gx[dz][dy];
+    }
+  double vy[2], gxy[2], gyy[2];
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    gyy[dz] = vx[dz][1] - vx[dz][0];
+    vy[dz] = vx[dz][0] + f[1] * gyy[dz];
+    gxy[dz] = gx[dz][0] + f[1] * (gx[dz][1] - gx[dz][0]);
+  }
+  const double v = vy[0] + f[2] * (vy[1] - vy[0]);
+  const double dfx = gxy[0] + f[2] * (gxy[1] - gxy[0]);
+  const double dfy = gyy[0] + f[2] * (gyy[1] - gyy[0]);
+  const double dfz = vy[1] - vy[0];
+  dvdp[0] = inside[0] ? dfx / G.h : 0.0;
+  dvdp[1] = inside[1] ? dfy / G.h : 0.0;
+  dvdp[2] = inside[2] ? dfz / G.h : 0.0;
+  return v;
+}
+
+// One pair term (i < j, different torsion groups) of the oracle's
+// orc_grid_score: sc and the energy term, in its operation order.
+__device__ __forceinline__ void strict_pair(const GridSmem& S, int i, int j, double& sc, double& e, d3& d) {
+  const double4 ri = S.xr[i], rj = S.xr[j];
+  d = {ri.x - rj.x, ri.y - rj.y, ri.z - rj.z};
+  const double4 ci = S.chem64[i], cj = S.chem64[j];
+  const double d0 = ci.x + cj.x;
+  const double c2 = 0.5625 * d0 * d0;
+  const double u = dot(d, d) + c2;
+  const double rho2 = (d0 * d0 + c2) / u;
+  const double rho6 = rho2 * rho2 * rho2;
+  const double rho12 = rho6 * rho6;
+  const double eps = sqrt(ci.y * cj.y);
+  const double qq = S.elec_scale * ci.z * cj.z;
+  e = eps * (rho12 - 2.0 * rho6) + qq / u;
+  sc = -12.0 * eps * (rho12 - rho6) / u - 2.0 * qq / (u * u);
+}
+
+// orc_grid_score (oracle/mdr_oracle.c) on the device, bit for bit: double
+// arithmetic in the oracle's order, correctly rounded trig, the oracle's
+// sequential sums (over atoms, over pairs in (i, j) order) run by single
+// threads.  A parity mode: per-run comparisons of grid dockings against the
+// oracle, at a fraction of the FP32 path's speed.
+__device__ __noinline__ GridEvalD grid_eval_strict(const GridSmem& S, const GridView& G, int buf, bool intra,
+                                                  bool bad_in, bool& bad_out) {
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int na = S.na, nr = S.nr, dim = 6 + nr;
+  double2* trig = S.trig[buf];
+  if (tid >= 3 && tid < dim) {
+    double s, c;
+    cr::sincos(S.g[tid], &s, &c);
+    trig[tid - 3] = make_double2(s, c);
+  }
+  bad_out = __syncthreads_or(bad_in) != 0;
+  GridEvalD out;
+  out.e = 0.0;
+  out.gd = 0.0;
+  if (bad_out) return out;
+  const double2 t1 = trig[0], t2 = trig[1], t3 = trig[2];
+  const Frame fr = frame_from_trig(t1.x, t1.y, t2.x, t2.y, t3.x, t3.y);
+  const d3 t = {S.g[0], S.g[1], S.g[2]};
+  for (int i = tid; i < na; i += T) {
+    const double4 at = S.atoms[i];
+    d3 local = {at.x, at.y, at.z};
+    const int k = S.tors[i];
+    if (k >= 0) {  // rotate_axis docking.cpp:57-60 (oracle: add3(add3(c v, s a x v), ((1 - c) a.v) a))
+      const d3 ax = {S.taxes[3 * k], S.taxes[3 * k + 1], S.taxes[3 * k + 2]};
+      const double2 sc = trig[3 + k];
+      local = (sc.y * local + sc.x * cross(ax, local)) + ((1.0 - sc.y) * dot(ax, local)) * ax;
+    }
+    const d3 r = mv(fr.R, local);
+    const d3 wp = t + r;
+    const double p[3] = {wp.x, wp.y, wp.z};
+    double dv[3], off[3];
+    double e = grid_sample_f64(G, S.type[i], at.w, S.chem64[i].z, p, dv, off);
+    double F[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      e += MDR_GRID_OUTSIDE_K * off[a] * off[a];
+      F[a] = dv[a] + 2.0 * MDR_GRID_OUTSIDE_K * off[a];
+    }
+    S.xr[i] = make_double4(r.x, r.y, r.z, 0.0);
+    S.xf[i] = make_double4(F[0], F[1], F[2], e);
+  }
+  __syncthreads();
+  if (intra) {
+    // atom a's intramolecular force in the oracle's update order: the pairs
+    // (i, a), i < a (subtracted), then (a, j), j > a (added); pair energies
+    // of row a stored for the sequential sum
+    for (int a = tid; a < na; a += T) {
+      d3 fi = {0.0, 0.0, 0.0};
+      const int ga = S.tors[a];
+      for (int i = 0; i < a; ++i) {
+        if (S.tors[i] == ga) continue;
+        double sc, e;
+        d3 d;
+        strict_pair(S, i, a, sc, e, d);
+        fi = fi - sc * d;
+      }
+      double* row = S.xep + (size_t)a * (2 * na - a - 1) / 2;
+      for (int j = a + 1; j < na; ++j) {
+        if (S.tors[j] == ga) continue;
+        double sc, e;
+        d3 d;
+        strict_pair(S, a, j, sc, e, d);
+        fi = fi + sc * d;
+        row[j - a - 1] = e;
+      }
+      S.xfi[a] = make_double4(fi.x, fi.y, fi.z, 0.0);
+    }
+  } else {
+    for (int a = tid; a < na; a += T) S.xfi[a] = make_double4(0.0, 0.0, 0.0, 0.0);
+  }
+  __syncthreads();
+  // the oracle's sequential sums: grid terms over atoms (thread 0), pair
+  // energies over (i, j) (thread 32, a second warp)
+  if (tid == 0) {
+    double e_inter = 0.0;
+    d3 gs = {0.0, 0.0, 0.0}, ts = {0.0, 0.0, 0.0};
+    for (int i = 0; i < na; ++i) {
+      const double4 f4 = S.xf[i], r4 = S.xr[i];
+      const d3 F = {f4.x, f4.y, f4.z};
+      e_inter += f4.w;
+      gs = gs + F;
+      ts = ts + cross(d3{r4.x, r4.y, r4.z}, F);
+    }
+    S.xtot[0] = e_inter;
+    S.xtot[1] = gs.x;
+    S.xtot[2] = gs.y;
+    S.xtot[3] = gs.z;
+    S.xtot[4] = ts.x;
+    S.xtot[5] = ts.y;
+    S.xtot[6] = ts.z;
+  }
+  if (tid == (T > 32 ? 32 : 0)) {
+    double e_intra = 0.0;
+    if (intra)
+      for (int i = 0; i < na; ++i) {
+        const double* row = S.xep + (size_t)i * (2 * na - i - 1) / 2;
+        const int gi = S.tors[i];
+        for (int j = i + 1; j < na; ++j)
+          if (S.tors[j] != gi) e_intra += row[j - i - 1];
+      }
+    S.xtot[7] = e_intra;
+  }
+  __syncthreads();
+  out.e = S.xtot[0] + S.xtot[7];
+  if (tid < dim) {
+    const d3 ts = {S.xtot[4], S.xtot[5], S.xtot[6]};
+    if (tid < 3) {
+      out.gd = S.xtot[1 + tid];
+    } else if (tid == 3) {
+      out.gd = dot(d3{0.0, 0.0, 1.0}, ts);
+    } else if (tid == 4) {
+      out.gd = dot(fr.ax_theta, ts);
+    } else if (tid == 5) {
+      out.gd = dot(fr.ax_alpha, ts);
+    } else {
+      const int k = tid - 6;
+      d3 tk = {0.0, 0.0, 0.0};
+      for (int i = 0; i < na; ++i)
+        if (S.tors[i] == k) {
+          const double4 f4 = S.xf[i], q4 = S.xfi[i], r4 = S.xr[i];
+          tk = tk + cross(d3{r4.x, r4.y, r4.z}, d3{f4.x, f4.y, f4.z} + d3{q4.x, q4.y, q4.z});
+        }
+      const d3 tw = mv(fr.R, d3{S.taxes[3 * k], S.taxes[3 * k + 1], S.taxes[3 * k + 2]});
+      out.gd = dot(tw, tk);
+    }
+  }
+  return out;
+}
 
 template <int METHOD>
-__device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView& G, int buf, bool intra, bool bad_in, bool& bad_out) {
+__device__ __forceinline__ GridEval grid_eval_fp32(const GridSmem& S, const GridView& G, int buf, bool intra, bool bad_in, bool& bad_out) {
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5;
   const int nr = S.nr, dim = 6 + nr;
   // A: angles owned by threads 3..dim-1
@@ -407,6 +667,16 @@ __device__ __forceinline__ GridEval grid_eval(const GridSmem& S, const GridView&
   return out;
 }
 
+template <int METHOD>
+__device__ __forceinline__ typename GridEvalT<METHOD>::type grid_eval(const GridSmem& S, const GridView& G, int buf,
+                                                                        bool intra, bool bad_in, bool& bad_out) {
+  if constexpr (METHOD == kGridStrict) {
+    return grid_eval_strict(S, G, buf, intra, bad_in, bad_out);
+  } else {
+    return grid_eval_fp32<METHOD>(S, G, buf, intra, bad_in, bad_out);
+  }
+}
+
 // ------------------------------------------------------- local search
 struct GridLs {
   double energy;
@@ -430,7 +700,7 @@ __device__ __forceinline__ GridLs grid_local_search(const GridSmem& S, const Gri
     S.best[tid] = x;
   }
   bool bad = false;
-  GridEval ev = grid_eval<METHOD>(S, G, 0, intra, false, bad);
+  auto ev = grid_eval<METHOD>(S, G, 0, intra, false, bad);
   GridLs r;
   r.energy = (double)ev.e;
   r.iterations = 0;
@@ -471,19 +741,23 @@ template <int METHOD>
 __global__ void grid_score_kernel(LigandView L, GridView G, FlexView F, const double* __restrict__ genos, int n,
                                   float* __restrict__ energy, float* __restrict__ grad, float* __restrict__ torque) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   const int item = blockIdx.x;
   const int dim = 6 + L.n_rot;
   if (threadIdx.x < dim) S.g[threadIdx.x] = genos[(size_t)item * dim + threadIdx.x];
   __syncthreads();
   bool bad;
-  const GridEval ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
-  if (threadIdx.x < dim) grad[(size_t)item * dim + threadIdx.x] = ev.gd;
+  const auto ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
+  if (threadIdx.x < dim) grad[(size_t)item * dim + threadIdx.x] = (float)ev.gd;
   if (threadIdx.x == 0) {
-    energy[item] = ev.e;
+    energy[item] = (float)ev.e;
     float t[3] = {0.f, 0.f, 0.f};
-    for (int w = 0; w < S.W; ++w)
-      for (int c = 0; c < 3; ++c) t[c] += S.wpart[w * 8 + 4 + c];
+    if constexpr (METHOD == kGridStrict) {
+      for (int c = 0; c < 3; ++c) t[c] = (float)S.xtot[4 + c];
+    } else {
+      for (int w = 0; w < S.W; ++w)
+        for (int c = 0; c < 3; ++c) t[c] += S.wpart[w * 8 + 4 + c];
+    }
     torque[3 * (size_t)item] = t[0];
     torque[3 * (size_t)item + 1] = t[1];
     torque[3 * (size_t)item + 2] = t[2];
@@ -495,7 +769,7 @@ __global__ void grid_ls_kernel(LigandView L, GridView G, FlexView F, const doubl
                                int max_iters, double tol, double* __restrict__ out_g, double* __restrict__ out_e,
                                int* __restrict__ out_it, int* __restrict__ out_cv, int* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   __syncthreads();
   const int item = blockIdx.x;
   const int dim = 6 + L.n_rot;
@@ -526,7 +800,7 @@ __global__ void grid_lga_init_kernel(GridLigands GL, GridView G, LgaDev D) {
   const int lig = run_ligand(GL, run);
   const LigandView L = GL.L[lig];
   const FlexView F = GL.F[lig];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   const int dim = 6 + L.n_rot;
   const int d = threadIdx.x;
   if (d < dim) {
@@ -539,7 +813,7 @@ __global__ void grid_lga_init_kernel(GridLigands GL, GridView G, LgaDev D) {
   }
   __syncthreads();
   bool bad;
-  const GridEval ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
+  const auto ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
   if (threadIdx.x == 0) D.pope[0][(size_t)run * D.P + p] = (double)ev.e;
 }
 
@@ -553,7 +827,7 @@ __global__ void grid_lga_offspring_kernel(GridLigands GL, GridView G, LgaDev D, 
   const int lig = run_ligand(GL, run);
   const LigandView L = GL.L[lig];
   const FlexView F = GL.F[lig];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   const int dim = 6 + L.n_rot;
   const int c = D.cur[run];
   const double* pop = D.pop[c] + (size_t)run * D.P * D.dim;
@@ -590,7 +864,7 @@ __global__ void grid_lga_offspring_kernel(GridLigands GL, GridView G, LgaDev D, 
   }
   __syncthreads();
   bool bad;
-  const GridEval ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
+  const auto ev = grid_eval<METHOD>(S, G, 0, F.intra != 0, false, bad);
   if (threadIdx.x == 0) ne[1 + i] = (double)ev.e;
 }
 
@@ -604,7 +878,7 @@ __global__ void grid_lga_ls_kernel(GridLigands GL, GridView G, LgaDev D) {
   const int lig = run_ligand(GL, run);
   const LigandView L = GL.L[lig];
   const FlexView F = GL.F[lig];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   const int dim = 6 + L.n_rot;
   if (threadIdx.x < 32) {
     const int t = ls_target(D, run, r);
@@ -634,7 +908,7 @@ __global__ void grid_lga_polish_kernel(GridLigands GL, GridView G, LgaDev D) {
   const int lig = run_ligand(GL, run);
   const LigandView L = GL.L[lig];
   const FlexView F = GL.F[lig];
-  const GridSmem S = grid_load(L, F, smem);
+  const GridSmem S = grid_load(L, F, smem, METHOD == kGridStrict);
   __syncthreads();
   if (D.status[run] != MDR_OK) return;
   const long long remaining = D.max_evals - D.evals[run];
@@ -703,6 +977,7 @@ static cudaError_t gprep(K kernel, size_t smem) {
     switch (method) {                                                                               \
       case MDR_METHOD_BASELINE: KERNEL<MDR_METHOD_BASELINE><<<g, b, smem, s>>>(args...); break;     \
       case MDR_METHOD_TCU: KERNEL<MDR_METHOD_TCU><<<g, b, smem, s>>>(args...); break;               \
+      case kGridStrict: KERNEL<kGridStrict><<<g, b, smem, s>>>(args...); break;                     \
       default: KERNEL<MDR_METHOD_TCU_SPLIT><<<g, b, smem, s>>>(args...); break;                     \
     }                                                                                               \
   }                                                                                                 \
@@ -710,6 +985,7 @@ static cudaError_t gprep(K kernel, size_t smem) {
     switch (method) {                                                                               \
       case MDR_METHOD_BASELINE: return gprep(KERNEL<MDR_METHOD_BASELINE>, smem);                    \
       case MDR_METHOD_TCU: return gprep(KERNEL<MDR_METHOD_TCU>, smem);                              \
+      case kGridStrict: return gprep(KERNEL<kGridStrict>, smem);                                    \
       default: return gprep(KERNEL<MDR_METHOD_TCU_SPLIT>, smem);                                    \
     }                                                                                               \
   }
@@ -721,11 +997,13 @@ MDR_GRID_DISPATCH(grid_lga_offspring_kernel)
 MDR_GRID_DISPATCH(grid_lga_ls_kernel)
 MDR_GRID_DISPATCH(grid_lga_polish_kernel)
 
-static size_t gsmem(const LigandView& L, const FlexView& F, int T) {
-  return grid_smem_bytes(L.n_atoms, L.n_rot, F.n_tors_atoms, T);
+static size_t gsmem(const LigandView& L, const FlexView& F, int T, int method) {
+  return grid_smem_bytes(L.n_atoms, L.n_rot, F.n_tors_atoms, T) + (method == kGridStrict ? grid_strict_bytes(L.n_atoms) : 0);
 }
 
-size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads) { return gsmem(L, F, threads); }
+size_t grid_smem_for(const LigandView& L, const FlexView& F, int threads, int method) {
+  return gsmem(L, F, threads, method);
+}
 size_t grid_smem_for(int n_atoms, int n_rot, int n_tors_atoms, int threads) {
   return grid_smem_bytes(n_atoms, n_rot, n_tors_atoms, threads);
 }
@@ -733,7 +1011,7 @@ size_t grid_smem_for(int n_atoms, int n_rot, int n_tors_atoms, int threads) {
 cudaError_t launch_grid_score(const LigandView& L, const GridView& G, const FlexView& F, const double* genos, int n,
                               int method, int threads, float* energy, float* grad, float* torque, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const size_t sm = gsmem(L, F, threads);
+  const size_t sm = gsmem(L, F, threads, method);
   cudaError_t e = gprep_grid_score_kernel(method, sm);
   if (e != cudaSuccess) return e;
   gdispatch_grid_score_kernel(method, n, threads, sm, s, L, G, F, genos, n, energy, grad, torque);
@@ -744,7 +1022,7 @@ cudaError_t launch_grid_local_search(const LigandView& L, const GridView& G, con
                                      int n, int max_iters, double tol, int method, int threads, double* out_g,
                                      double* out_e, int* out_it, int* out_cv, int* status, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const size_t sm = gsmem(L, F, threads);
+  const size_t sm = gsmem(L, F, threads, method);
   cudaError_t e = gprep_grid_ls_kernel(method, sm);
   if (e != cudaSuccess) return e;
   gdispatch_grid_ls_kernel(method, n, threads, sm, s, L, G, F, starts, n, max_iters, tol, out_g, out_e, out_it,

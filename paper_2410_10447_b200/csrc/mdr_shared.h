@@ -65,6 +65,8 @@ struct GridView {
 struct FlexView {
   const int* type;
   const float4* chem;
+  const double4* chem64;  // {radius, epsilon, charge, 0} in double (strict FP64 grid mode; single-ligand calls)
+  double elec_scale;
   const int* grp_off;    // n_rot + 1
   const int* grp_atoms;  // n_tors_atoms
   int n_tors_atoms, intra;

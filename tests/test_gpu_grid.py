@@ -188,3 +188,93 @@ def test_c4_full_size_maps_and_scores(port, dev):
         we, wg, _, _ = port.grid_score(inst, G, params, p)
         assert abs(e[i] - we) <= 1e-5 * max(1.0, abs(we))
         assert np.abs(g[i] - wg).max() <= 2e-5 * max(1.0, np.abs(wg).max())
+
+
+# ---- strict FP64 grid mode (context pair precision MDR_PAIR_FP64): the
+# oracle's double arithmetic in the oracle's order with correctly rounded
+# trig on both sides (csrc/crmath.cuh, oracle/crmath.h), so dockings are
+# compared run for run, bit for bit.
+@pytest.fixture(scope="module")
+def strict_dev():
+    from paper_2410_10447_b200 import PAIR_FP64, Device
+
+    d = Device(0, pair=PAIR_FP64)
+    yield d
+    d.close()
+
+
+def test_crmath_device_equals_oracle(dev):
+    """csrc/crmath.cuh (device) and oracle/crmath.h compute the same
+    correctly rounded sin / cos / log bit for bit (10^6 inputs)."""
+    import ctypes as C
+
+    from oracle.oracle import cr_values
+
+    n = 1 << 20
+    out = np.zeros((n, 8))
+    assert dev.lib.mdr_crmath_values(dev.ctx, 0, n, C.c_void_p(out.ctypes.data)) == 0
+    want = cr_values(0, n)
+    assert np.array_equal(out[:, :4].view(np.uint64), want.view(np.uint64))
+
+
+def test_grid_strict_local_search_identical(port, strict_dev, small):
+    inst, lp, G, _ = small
+    dg = strict_dev.grid_upload(G)
+    starts = _poses(inst, 24, 5, spread=2.0)
+    res = strict_dev.grid_local_search_batch(dg, inst, lp, starts, 150, 1e-4, BASELINE, 64)
+    for s, r in zip(starts, res):
+        w = port.grid_local_search(inst, G, lp, s, 150, 1e-4)
+        assert r.energy == w["energy"] and r.iterations == w["iterations"]
+        assert np.array_equal(r.genotype, w["genotype"])
+    dg.free()
+
+
+def test_grid_strict_lga_identical(port, strict_dev, small, large):
+    """Whole grid-mode LGA runs (init, offspring with correctly rounded
+    Box-Muller draws, Lamarckian searches, polish): the device's strict path
+    equals orc_grid_lga_run run for run, with and without intramolecular
+    terms, small and 100-atom / 30-torsion ligands."""
+    for case, gens in ((small, 4), (large, 2)):
+        inst, lp, G, _ = case
+        dg = strict_dev.grid_upload(G)
+        s = LgaSettings(generations=gens)
+        seeds = np.arange(4, dtype=np.uint64) + 2000
+        gpu = strict_dev.grid_lga_run_batch(dg, inst, lp, BASELINE, s, seeds)
+        for r, sd in zip(gpu, seeds):
+            w = port.grid_lga_run(inst, G, lp, s, int(sd))
+            assert r.best_energy == w["best_energy"] and r.evaluations == w["evaluations"], (sd, r.best_energy, w)
+            assert np.array_equal(r.best_genotype, w["best_genotype"])
+            assert [x[0] for x in r.runs] == [x[0] for x in w["runs"]]
+        dg.free()
+
+
+def test_c4_grid_strict_runs_identical_to_oracle():
+    """C4 at full size (100 atoms / 30 torsions, 126^3 x 6 device-built maps,
+    intramolecular on, default LgaSettings, partition 64), 16 paired seeds:
+    the strict FP64 device docking reproduces orc_grid_lga_run run for run
+    (best energy, evaluations, genotype) and the 2 A clustering of the final
+    poses is identical (north_star: "final best-pose energies and RMSD
+    clustering must match")."""
+    from oracle.oracle import Oracle, grid_lga_runs_parallel
+    from paper_2410_10447_b200 import PAIR_FP64, Device
+    from paper_2410_10447_b200._abi import Grid
+    from paper_2410_10447_b200.workloads import c4
+
+    inst, params, fields, grid, s = c4()
+    d = Device(0, pair=PAIR_FP64)
+    try:
+        dg = d.grid_build(inst, fields, grid)
+        G = Grid(grid.shape, grid.n_types, grid.origin, grid.spacing, dg.download())
+        seeds = np.arange(16, dtype=np.uint64) + np.uint64(515000)
+        gpu = d.grid_lga_run_batch(dg, inst, params, BASELINE, s, seeds)
+        cpu = grid_lga_runs_parallel(inst, G, params, s, seeds)
+        for g, c in zip(gpu, cpu):
+            assert g.best_energy == c[0] and g.evaluations == c[1]
+            assert np.array_equal(g.best_genotype, c[3])
+        ge = np.array([g.best_energy for g in gpu])
+        gc, _, gn = d.cluster_poses(inst, np.stack([g.best_genotype for g in gpu]), ge, 2.0)
+        cc, _, cn = Oracle("port").cluster_poses(inst, np.stack([c[3] for c in cpu]), np.array([c[0] for c in cpu]), 2.0)
+        assert gn == cn and np.array_equal(gc, cc)
+        dg.free()
+    finally:
+        d.close()

@@ -157,3 +157,35 @@ def test_grid_lga_is_deterministic_and_tracks_best(port, small):
     assert np.array_equal(a["best_genotype"], b["best_genotype"])
     assert a["best_energy"] <= min(r[0] for r in a["runs"])
     assert port.grid_score(inst, G, lp, a["best_genotype"])[0] == pytest.approx(a["best_energy"], rel=1e-12)
+
+
+def test_grid_oracle_correctly_rounded_math():
+    """The grid-mode oracle's sin / cos / log (oracle/crmath.h, correctly
+    rounded) agree with glibc except where glibc itself is not correctly
+    rounded (~0.1 % of calls), and then by one ulp."""
+    import math
+
+    from oracle.oracle import cr_values
+
+    n = 20000
+    v = cr_values(0, n)
+    mix = lambda z: _mix64(z)  # noqa: E731
+    off = 0
+    for i in range(n):
+        a = -math.pi + 2.0 * math.pi * ((mix(((4 * i + 1) * 0x9E3779B97F4A7C15) & M64) >> 11) * 2.0**-53)
+        u1 = ((mix(((4 * i + 2) * 0x9E3779B97F4A7C15) & M64) >> 11) + 1) * 2.0**-53
+        z = 2.0 * math.pi * ((mix(((4 * i + 3) * 0x9E3779B97F4A7C15) & M64) >> 11) * 2.0**-53)
+        for got, want in zip(v[i], (math.sin(a), math.cos(a), math.log(u1), math.cos(z))):
+            if got != want:
+                off += 1
+                assert abs(got - want) <= math.ulp(want), (i, got, want)
+    assert off <= 0.01 * 4 * n, off
+
+
+M64 = (1 << 64) - 1
+
+
+def _mix64(z):
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9 & M64
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EB & M64
+    return z ^ (z >> 31)

@@ -6,6 +6,11 @@ N paired seeds on the device (FP32) and by the double-precision oracle
 (orc_grid_lga_run, one process per host core).  Reports the paired-seed
 mean-best difference, the best energies and the 2 A clustering of the final
 poses.  Writes gpurun_out/grid_parity_scale.json.
+
+GRID_STRICT=1: the device runs the strict FP64 grid path (context pair
+precision MDR_PAIR_FP64: the oracle's double arithmetic and order, correctly
+rounded trig on both sides) and the report counts runs identical to the
+oracle (best energy and evaluation count) and times the device docking.
 """
 import json
 import multiprocessing as mp
@@ -35,13 +40,21 @@ def main():
     from paper_2410_10447_b200._abi import Grid
     from paper_2410_10447_b200.workloads import c4
 
+    from paper_2410_10447_b200 import PAIR_FP32, PAIR_FP64
+
+    strict = os.environ.get("GRID_STRICT") == "1"
     inst, params, fields, grid, s = c4()
-    dev = Device(0)
+    dev = Device(0, pair=PAIR_FP64 if strict else PAIR_FP32)
     dg = dev.grid_build(inst, fields, grid)
     G = Grid(grid.shape, grid.n_types, grid.origin, grid.spacing, dg.download())
     _G["case"] = (inst, params, G, s)
     seeds = np.arange(N, dtype=np.uint64) + np.uint64(BASE)
+    import time
+
     gpu = dev.grid_lga_run_batch(dg, inst, params, BASELINE, s, seeds)
+    t0 = time.perf_counter()
+    gpu = dev.grid_lga_run_batch(dg, inst, params, BASELINE, s, seeds)
+    dt = time.perf_counter() - t0
     with mp.get_context("fork").Pool(os.cpu_count()) as pool:
         cpu = sorted(pool.map(_cpu, [int(x) for x in seeds]))
     ge = np.array([r.best_energy for r in gpu])
@@ -59,11 +72,15 @@ def main():
            "diff_of_means_in_standard_errors": float(abs(ge.mean() - ce.mean()) /
                                                      np.sqrt(ge.var(ddof=1) / N + ce.var(ddof=1) / N)),
            "clusters_gpu": int(gn), "clusters_oracle": int(cn),
+           "clusters_identical": bool(gn == cn and np.array_equal(gc, cc)),
+           "identical_runs": int(sum(g.best_energy == c[1] and g.evaluations == c[2] for g, c in zip(gpu, cpu))),
+           "device_mode": "strict FP64 (MDR_PAIR_FP64)" if strict else "FP32 grid path",
+           "device_evals_per_s": float(sum(r.evaluations for r in gpu) / dt),
            "evals_gpu_mean": float(np.mean([r.evaluations for r in gpu])),
            "evals_oracle_mean": float(np.mean([c[2] for c in cpu]))}
     print(json.dumps(out, indent=1))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "grid_parity_scale.json"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", os.environ.get("GRID_PARITY_OUT", "grid_parity_scale.json")), "w") as f:
         json.dump(out, f, indent=1)
 
 
