@@ -236,7 +236,10 @@ void pick_chunks(int na, int ns, int search_lanes, int force_len, int& n_chunks,
 // G = 1, len 8 -> 160 items, 3 rounds x 8; G = 3, len 8 -> 56 items, 1
 // round x 24: equal path and a third of the site loads, but measured
 // 200.3 vs 179.9 M evals/s (G = 3 holds 6 pair terms in flight per lane at
-// 128 registers, G = 1 eight; profiles/r2_ls_multi_ab.json).
+// 128 registers, G = 1 eight; profiles/r2_ls_multi_ab.json).  Up to 512
+// (atom, chunk) items (C4 analytic, 100 atoms x 64 sites: 4 chunks of 16,
+// 54.6 M evals/s against 51.3 M with the warp-per-pose kernels' 256-item
+// limit, 2 chunks of 32).
 void pick_search_items(int na, int ns, int force_len, int force_group, int& n_chunks, int& chunk_len, int& group) {
   constexpr int kBatch = 8;
   n_chunks = 1;
@@ -256,7 +259,7 @@ void pick_search_items(int na, int ns, int force_len, int force_group, int& n_ch
     if (force_group > 0 && G != force_group) continue;
     for (int len = kBatch; len < ns; len += kBatch) {
       const int n = (ns + len - 1) / len;
-      if (na * n > kMaxChunkItems || na * n <= 32) continue;
+      if (na * n > kMaxChunkItemsForced || na * n <= 32) continue;  // the search's own part buffers
       const int items = (na + G - 1) / G * n;
       const long cost = (long)((items + 63) / 64) * G * len;
       if (cost < best) {

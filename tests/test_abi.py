@@ -64,7 +64,8 @@ def test_site_chunking_policy():
             for ns in (8, 30, 64, 200):
                 n, ln, g = pick_search(PAIR_FP64_FAST, na, ns, warps, group=True)
                 if n > 1:
-                    assert ln % 8 == 0 and na * n <= 256 and (n - 1) * ln < ns <= n * ln
+                    # the warp-per-pose policy stages at most 256 items, the two-warp search 512
+                    assert ln % 8 == 0 and na * n <= (256 if warps == 1 else 512) and (n - 1) * ln < ns <= n * ln
                     if warps == 1:
                         assert g == 1 and ((na * n + 31) // 32) * (ln + 4) < ((na + 31) // 32) * ns
                     else:

@@ -321,7 +321,8 @@ def test_multi_warp_search_bit_identical(instances, monkeypatch, warps, group):
     two warps (ls_multi.cu, warps = 2; 0 = the legacy warp-pair kernel): the
     helper takes chunk items of every evaluation, the leader keeps the
     genotype in registers; an item is one chunk of sites against 1 or 3
-    atoms.  Same items, same arithmetic, same
+    atoms; ligands past 32 atoms or 32 dimensions run the kernel's BIG form
+    (C4 analytic, a 40-torsion ligand).  Same items, same arithmetic, same
     combine order as the one-warp kernel, so with the same site chunking
     (pinned here: MDR_CHUNK_LEN = MDR_LS_CHUNK_LEN = 8) whole LGA runs are
     bit-identical.  Covers a 40-torsion ligand (dim 46 > 32: the multi-warp
@@ -336,13 +337,18 @@ def test_multi_warp_search_bit_identical(instances, monkeypatch, warps, group):
     assert multi.lib.mdr_ctx_set_ls_warps(multi.ctx, warps) == 0
     single = Device(0, pair=PAIR_FP64_FAST)
     assert single.lib.mdr_ctx_set_ls_warps(single.ctx, 1) == 0
+    from paper_2410_10447_b200.workloads import c4_analytic
+
     rng = derive_rng(93, "pair/identity")
-    cases = [c3(), random_instance(rng, 3, 28, 64), random_instance(rng, 40, 16, 64)]
-    seeds = np.arange(16, dtype=np.uint64) + np.uint64(4321)
-    for inst in cases:
+    c4a, c4s = c4_analytic()
+    cases = [(c3(), LgaSettings(), 16), (random_instance(rng, 3, 28, 64), LgaSettings(), 16),
+             (random_instance(rng, 40, 16, 64), LgaSettings(), 16),  # dim 46: two dimensions per lane
+             (c4a, c4s, 4)]  # 100 atoms: atoms in blocks of 32
+    for inst, st, n_seeds in cases:
+        seeds = np.arange(n_seeds, dtype=np.uint64) + np.uint64(4321)
         for method in (BASELINE, TCU_SPLIT, TCU):
-            a = multi.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
-            b = single.lga_run_batch(inst, method, SINGLE, LgaSettings(), seeds)
+            a = multi.lga_run_batch(inst, method, SINGLE, st, seeds)
+            b = single.lga_run_batch(inst, method, SINGLE, st, seeds)
             for x, y in zip(a, b):
                 assert x.best_energy == y.best_energy and x.evaluations == y.evaluations
                 assert np.array_equal(x.best_genotype, y.best_genotype)
