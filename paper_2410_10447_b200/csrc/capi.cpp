@@ -323,9 +323,10 @@ int mdr_phase_prof(uint64_t* out16, int reset) {
 int mdr_phase_prof_sm(uint32_t* out256, int reset) {
   if (!out256) return fail(nullptr, MDR_ERR_INVALID, "null argument");
   unsigned v[256];
-  if (!sm_searches_read(v, reset != 0))
+  unsigned gv[256];
+  if (!sm_searches_read(v, reset != 0) || !sm_grid_read(gv, reset != 0))
     return fail(nullptr, MDR_ERR_INVALID, "not a phase-profiling build (-DMDR_PHASE_PROF=1)");
-  for (int k = 0; k < 256; ++k) out256[k] = v[k];
+  for (int k = 0; k < 256; ++k) out256[k] = v[k] + gv[k];  // analytic two-warp search + grid-mode search
   return MDR_OK;
 }
 

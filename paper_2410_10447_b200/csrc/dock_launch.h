@@ -65,6 +65,7 @@ cudaError_t launch_crmath_probe(long long i0, int n, double* out, cudaStream_t s
 bool phase_prof_read(unsigned long long* out16, bool reset);
 bool phase_prof_read_multi(unsigned long long* out16, bool reset);  // adds ls_multi.cu's counters
 bool sm_searches_read(unsigned* out256, bool reset);  // searches per SM (phase-profiling builds)
+bool sm_grid_read(unsigned* out256, bool reset);      // grid-mode LGA searches per SM (phase-profiling builds)
 cudaError_t launch_fill_uniform(uint64_t key, long long n, float* out, cudaStream_t s);
 cudaError_t launch_ddiv_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 cudaError_t launch_sincos_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);

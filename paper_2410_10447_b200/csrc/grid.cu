@@ -868,11 +868,22 @@ __global__ void grid_lga_offspring_kernel(GridLigands GL, GridView G, LgaDev D, 
   if (threadIdx.x == 0) ne[1 + i] = (double)ev.e;
 }
 
+#if MDR_PHASE_PROF
+__device__ unsigned int g_sm_grid[256];  // grid LGA searches started per SM (phase-profiling builds)
+#endif
+
 template <int METHOD>
 __global__ void grid_lga_ls_kernel(GridLigands GL, GridView G, LgaDev D) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_target;
   const int item = blockIdx.x;
+#if MDR_PHASE_PROF
+  if (threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    atomicAdd(&g_sm_grid[sm & 255], 1u);
+  }
+#endif
   const int run = item / D.L, r = item % D.L;
   if (!D.active[run]) return;
   const int lig = run_ligand(GL, run);
@@ -1061,6 +1072,21 @@ cudaError_t launch_grid_lga(const GridLigands& GL, size_t sm, const GridView& G,
   launches += 1;
   if (n_launches) *n_launches = launches;
   return cudaGetLastError();
+}
+
+bool sm_grid_read(unsigned* out256, bool reset) {
+#if MDR_PHASE_PROF
+  if (cudaMemcpyFromSymbol(out256, g_sm_grid, sizeof(unsigned) * 256) != cudaSuccess) return false;
+  if (reset) {
+    unsigned z[256] = {};
+    if (cudaMemcpyToSymbol(g_sm_grid, z, sizeof(z)) != cudaSuccess) return false;
+  }
+  return true;
+#else
+  (void)out256;
+  (void)reset;
+  return false;
+#endif
 }
 
 cudaError_t launch_grid_build(const GridView& G, const double* sites, int n_sites, const double* charge,
