@@ -132,17 +132,19 @@ int mdr_ctx_set_exact_torsion(mdr_ctx* ctx, int on);
  * LGA init / offspring, one-warp search, polish); *n_chunks = 1 means lane
  * per atom (always the case for the other pair modes).  DESIGN.md §3. */
 int mdr_site_chunking(int pair_precision, int n_atoms, int n_sites, int* n_chunks, int* chunk_len);
-/* The same policy for the LGA's Lamarckian search on `warps` (1 or 2) warps
- * per search (the default context runs 2, mdr_ctx_set_ls_warps).  On two
- * warps an item is (chunk, group of *atoms_per_item atoms): 1, or 3 when
- * register blocking shortens nothing on the critical path but cuts the
- * shared-memory site loads (C3: 8 chunks of 8 sites, 3 atoms per item). */
+/* The same policy for the LGA's Lamarckian search in form `warps` (1 = one
+ * warp; 2 and 3 = the multi-warp forms of mdr_ctx_set_ls_warps, which share
+ * one policy).  In the multi-warp forms an item is (chunk, group of
+ * *atoms_per_item atoms): 1, or 3 when register blocking shortens nothing on
+ * the critical path but cuts the shared-memory site loads. */
 int mdr_search_chunking(int pair_precision, int n_atoms, int n_sites, int warps, int* n_chunks, int* chunk_len,
                         int* atoms_per_item);
-/* Warps per Lamarckian search of the LGA (default 2 = the leader/helper
- * search of ls_multi.cu; 1 = one warp per search, 0 = the legacy warp-pair
- * kernel; env MDR_LS_WARPS).  Every choice gives bit-identical results for
- * the same chunking.  Set before the first docking of the context. */
+/* Form of the LGA's Lamarckian search (env MDR_LS_WARPS): 3 (default) = one
+ * leader warp per search plus a pool of item warps shared by the CTA's
+ * searches (ls_multi.cu); 2 = a leader and a dedicated helper warp per
+ * search; 1 = one warp per search; 0 = the legacy warp-pair kernel.  Every
+ * choice gives bit-identical results for the same chunking.  Set before the
+ * first docking of the context. */
 int mdr_ctx_set_ls_warps(mdr_ctx* ctx, int warps);
 /* Message of the last failing call on this context (thread-local copy). */
 const char* mdr_last_error(mdr_ctx* ctx);

@@ -56,7 +56,8 @@ struct mdr_ctx {
   int chunk_len = 0;  // > 0: pin the chunk length (MDR_CHUNK_LEN, timing only)
   int ls_pair = 1;    // warp-pair Lamarckian searches (MDR_LS_PAIR=0 disables)
   int tc05 = 1;       // TcuSplit batched reductions on tcgen05 where they win (MDR_TC05=0 disables)
-  int ls_warps = 2;   // warps per LGA Lamarckian search: 2 = ls_multi.cu, 1 = one warp, 0 = legacy pair kernel (MDR_LS_WARPS)
+  int ls_warps = 3;   // LGA Lamarckian search form (MDR_LS_WARPS): 3 = ls_multi.cu leaders + shared item-warp pool,
+                      // 2 = ls_multi.cu leader + helper warp, 1 = one warp, 0 = legacy pair kernel
   int ls_chunk_len = 0;  // > 0: pin the search's chunk length (MDR_LS_CHUNK_LEN, timing only)
   int ls_group = 0;      // > 0: pin the search's atoms per item (MDR_LS_GROUP: 1 or 3)
 
@@ -290,7 +291,7 @@ LigandView launch_view(const mdr_ctx* c, const mdr_dev_instance* di) {
   if (c->pair == MDR_PAIR_FP64_FAST && c->chunking) {
     pick_chunks(L.n_atoms, L.n_sites, 32, c->chunk_len, L.n_chunks, L.chunk_len);
     const int force = c->ls_chunk_len > 0 ? c->ls_chunk_len : c->chunk_len;
-    if (multi && c->ls_warps == 2)
+    if (multi && c->ls_warps >= 2)
       pick_search_items(L.n_atoms, L.n_sites, force, c->ls_group, L.ls_n_chunks, L.ls_chunk_len, L.ls_group);
     else
       pick_chunks(L.n_atoms, L.n_sites, search_lanes, force, L.ls_n_chunks, L.ls_chunk_len);
@@ -378,21 +379,22 @@ int mdr_ctx_set_cta_warps(mdr_ctx* c, int w) {
 }
 
 int mdr_ctx_set_ls_warps(mdr_ctx* c, int w) {
-  if (!c || w < 0 || w > 2) return fail(c, MDR_ERR_INVALID, "search warps must be 0..2 (0 = legacy warp pair)");
+  if (!c || w < 0 || w > 3)
+    return fail(c, MDR_ERR_INVALID, "search form must be 0..3 (3 = item-warp pool, 2 = helper, 1 = one warp, 0 = legacy pair)");
   c->ls_warps = w;
   c->ls_pair = w != 1;
   return MDR_OK;
 }
 
 int mdr_search_chunking(int pair, int na, int ns, int warps, int* n_chunks, int* chunk_len, int* atoms_per_item) {
-  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || warps < 1 || warps > 2 || pair < MDR_PAIR_FP64 ||
+  if (!n_chunks || !chunk_len || na < 0 || ns < 0 || warps < 1 || warps > 3 || pair < MDR_PAIR_FP64 ||
       pair > MDR_PAIR_FP64_FAST)
     return fail(nullptr, MDR_ERR_INVALID, "bad argument");
   *n_chunks = 1;
   *chunk_len = ns;
   int group = 1;
   if (pair == MDR_PAIR_FP64_FAST) {
-    if (warps == 2)
+    if (warps >= 2)
       pick_search_items(na, ns, 0, 0, *n_chunks, *chunk_len, group);
     else
       pick_chunks(na, ns, 32, 0, *n_chunks, *chunk_len);

@@ -35,7 +35,7 @@ struct LigandView {
   int n_chunks;       // FP64-fast: sites split into n_chunks ranges of chunk_len (1 = lane per atom)
   int chunk_len;
   int ls_pair;        // 1: Lamarckian searches may run on several warps (MDR_LS_PAIR=0: one warp)
-  int ls_warps;       // warps per Lamarckian search of the LGA (ls_multi.cu); 1 = the one-warp kernel
+  int ls_warps;       // Lamarckian search form of the LGA (mdr_ctx_set_ls_warps): 3 pool, 2 helper, 1 one warp, 0 legacy
   int ls_n_chunks;    // site chunking of that search (its own lane count), see capi.cpp pick_chunks
   int ls_chunk_len;
   int pad_;

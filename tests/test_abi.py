@@ -53,6 +53,7 @@ def test_site_chunking_policy():
     assert pick(PAIR_FP64_FAST, 20, 64) == (3, 24)  # C3 on one warp: 60 items in 2 rounds of 24 sites
     # C3's search on 2 warps: 8 chunks of 8 sites, one atom per item (160 items, 3 rounds of 64 lanes)
     assert pick_search(PAIR_FP64_FAST, 20, 64, 2, group=True) == (8, 8, 1)
+    assert pick_search(PAIR_FP64_FAST, 20, 64, 3, group=True) == (8, 8, 1)  # the pooled form: same policy
     assert pick_search(PAIR_FP64_FAST, 20, 64, 1) == pick(PAIR_FP64_FAST, 20, 64)
     assert pick(PAIR_FP64, 20, 64) == (1, 64)
     assert pick(PAIR_FP32, 20, 64) == (1, 64)
@@ -71,6 +72,6 @@ def test_site_chunking_policy():
                     else:
                         assert g in (1, 3) and na * n > 32
                         assert ((-(-na // g) * n + 63) // 64) * g * ln < ((na + 31) // 32) * ns
-    assert lib.mdr_search_chunking(PAIR_FP64_FAST, 20, 64, 3, ctypes.byref(ctypes.c_int()),
+    assert lib.mdr_search_chunking(PAIR_FP64_FAST, 20, 64, 4, ctypes.byref(ctypes.c_int()),
                                    ctypes.byref(ctypes.c_int()), None) != 0
     assert lib.mdr_site_chunking(7, 20, 64, ctypes.byref(ctypes.c_int()), ctypes.byref(ctypes.c_int())) != 0

@@ -315,11 +315,13 @@ def test_chunked_site_mapping_matches_lane_per_atom(port, instances, monkeypatch
     lane.close()
 
 
-@pytest.mark.parametrize("warps,group", [(0, 0), (2, 1), (2, 3)])
+@pytest.mark.parametrize("warps,group", [(0, 0), (2, 1), (2, 3), (3, 0), (3, 1)])
 def test_multi_warp_search_bit_identical(instances, monkeypatch, warps, group):
     """FP64-fast chunked ligands run each Lamarckian search of the LGA on
-    two warps (ls_multi.cu, warps = 2; 0 = the legacy warp-pair kernel): the
-    helper takes chunk items of every evaluation, the leader keeps the
+    several warps (ls_multi.cu: warps = 3, a leader per search and a pool of
+    item warps shared by the CTA's searches; warps = 2, a leader and a
+    helper; 0 = the legacy warp-pair kernel): the pool or the helper takes
+    chunk items of every evaluation, the leader keeps the
     genotype in registers; an item is one chunk of sites against 1 or 3
     atoms; ligands past 32 atoms or 32 dimensions run the kernel's BIG form
     (C4 analytic, a 40-torsion ligand).  Same items, same arithmetic, same

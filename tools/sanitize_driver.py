@@ -45,11 +45,11 @@ ligs, prms = zip(*[c5_ligand(j, sites) for j in range(3)])
 dev.grid_screen_batch(dg, list(ligs), list(prms), 2, BASELINE,
                       LgaSettings(generations=1, population_size=6, ls_max_iters=6, partition=64),
                       np.arange(6, dtype=np.uint64), 2.0)
-# chunked small ligand: the two-warp persistent search (ls_multi.cu), its
+# chunked small ligand: the multi-warp persistent search (ls_multi.cu: pooled and leader + helper), its
 # polish, and the one-warp / legacy-pair configurations
 from paper_2410_10447_b200.workloads import c3  # noqa: E402
 
-for warps in (2, 1, 0):
+for warps in (3, 2, 1, 0):
     d = Device(0, pair=PAIR_FP64_FAST)
     assert d.lib.mdr_ctx_set_ls_warps(d.ctx, warps) == 0
     for m, acc in ((BASELINE, SINGLE), (TCU_SPLIT, SINGLE)):
