@@ -462,8 +462,9 @@ def run_gpu_arm(args):
             flops = flop_per_eval(inst, settings.partition) * ls_evals.value
             achieved = flops / (ls_ms.value * 1e-3) / 1e12
             n_ls_launches = settings.generations + 1
-            roof = {"bound": "fp64", "kernel": "lga_ls_multi_kernel (device ADADELTA chain, leader + helper warp per search, "
-                                               "persistent over each generation's searches)",
+            roof = {"bound": "fp64", "kernel": "lga_ls_multi_kernel (device ADADELTA chain, pooled form: a leader warp per "
+                                               "search + a CTA-wide pool of item warps, persistent over each "
+                                               "generation's searches)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": "measured live: DFMA-chain kernel on this GPU (MEASURED_PEAKS.json has no FP64 "
                                    "figure)",

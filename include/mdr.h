@@ -495,8 +495,9 @@ int mdr_lga_batch_cluster(mdr_ctx* ctx, mdr_lga_batch* b, double rmsd_tol, int32
  * an experiment build with -DMDR_PHASE_PROF=1 records them; the product
  * build returns MDR_ERR_INVALID. */
 int mdr_phase_prof(uint64_t* out16, int reset);
-/* Searches of the two-warp LGA search started per SM (index = %smid) since
- * the last reset; phase-profiling builds only. */
+/* LGA searches started per SM (index = %smid) since the last reset: the
+ * multi-warp analytic search plus the grid-mode search; phase-profiling
+ * builds only. */
 int mdr_phase_prof_sm(uint32_t* out256, int reset);
 
 #ifdef __cplusplus

@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
 #include <cstdlib>
 
 #include "dock_launch.h"
@@ -1736,6 +1737,8 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instanc
   if (int rc = check_lga(ctx, method, s)) return rc;
   if (n_lig == 0 || runs == 0) return MDR_OK;
   const int T = s->partition;
+  static const bool timing = std::getenv("MDR_SCREEN_TIMING") != nullptr;  // host-pack / total split (stderr)
+  const auto t_start = std::chrono::steady_clock::now();
   // ---- validate and pack every ligand into one host image of the device block
   struct Lay {
     size_t atoms, taxes, box, tors, type, chem, off, mem;
@@ -1829,6 +1832,7 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instanc
     }
     seg[n_lig] = R;
   }
+  const auto t_packed = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(base, img.data(), img.size(), cudaMemcpyHostToDevice, S(ctx)));
   b->grid = true;
   b->G = g->view;
@@ -1880,6 +1884,12 @@ int mdr_grid_screen_batch(mdr_ctx* ctx, const mdr_dev_grid* g, const mdr_instanc
       for (int k = 0; k < runs; ++k, o += dim)
         std::memcpy(best_g + o, bg.data() + (size_t)(j * runs + k) * b->D.dim, sizeof(double) * dim);
     }
+  }
+  if (timing) {
+    const auto t_end = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "mdr_grid_screen_batch: %d ligands, host pack %.1f ms, total %.1f ms\n", n_lig,
+                 std::chrono::duration<double, std::milli>(t_packed - t_start).count(),
+                 std::chrono::duration<double, std::milli>(t_end - t_start).count());
   }
   for (int r = 0; r < R; ++r)
     if (status[r] != MDR_OK) return fail(ctx, status[r], "adadelta_step: non-finite gradient component");

@@ -14,8 +14,11 @@ namespace mdr {
 #ifndef MDR_LS_LB
 #define MDR_LS_LB 1
 #endif
+#ifndef MDR_LS_MAXT
+#define MDR_LS_MAXT 512  // threads per CTA the register allocation is sized for
+#endif
 #if MDR_LS_LB > 0
-#define MDR_LS_BOUNDS __launch_bounds__(512, MDR_LS_LB)
+#define MDR_LS_BOUNDS __launch_bounds__(MDR_LS_MAXT, MDR_LS_LB)
 #else
 #define MDR_LS_BOUNDS
 #endif

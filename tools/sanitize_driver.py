@@ -55,6 +55,11 @@ for warps in (3, 2, 1, 0):
     for m, acc in ((BASELINE, SINGLE), (TCU_SPLIT, SINGLE)):
         d.lga_run_batch(c3(), m, acc, LgaSettings(generations=2, ls_max_iters=20), [11, 12, 13])
     d.close()
+# the pooled search's BIG form (dim 46 > 32: two dimensions per leader lane)
+d = Device(0, pair=PAIR_FP64_FAST)
+big = random_instance(derive_rng(5, "san/big"), 40, 16, 64)
+d.lga_run_batch(big, BASELINE, SINGLE, LgaSettings(generations=2, ls_max_iters=12), [21, 22])
+d.close()
 # TcuSplit batches routed to tcgen05 (float4 and Partial7 forms, ragged tail)
 n_red = 148 * 32 + 5
 assert dev.lib.mdr_reduce_uses_tc05(dev.ctx, TCU_SPLIT, 32, n_red) == 1
