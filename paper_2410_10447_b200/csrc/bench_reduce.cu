@@ -341,14 +341,41 @@ __global__ void chain_kernel(const float4* __restrict__ in, int steps, float4* _
   }
 }
 
+#ifndef MDR_STREAM_PREFETCH
+#define MDR_STREAM_PREFETCH 0  // input sets in flight per thread (0: load at use)
+#endif
+// Streaming: block b reduces sets b, b + grid, ...; each thread keeps
+// MDR_STREAM_PREFETCH sets' float4 loads in flight (the one being reduced
+// and the next ones) (the block barriers of the reduction would otherwise
+// drain the memory pipe between sets).
 template <int K>
 __global__ void stream_kernel(const float4* __restrict__ in, int n_red, float4* __restrict__ out) {
   __shared__ Smem sm;
   sm.tile = reinterpret_cast<__half*>(g_dyn);
   sm.stage = reinterpret_cast<float*>(g_dyn);
+  constexpr int P = MDR_STREAM_PREFETCH;
+  if constexpr (P == 0) {  // load at use
+    int it = 0;
+    for (int r = blockIdx.x; r < n_red; r += gridDim.x, ++it) {
+      const float4 s = reduce_once<K>(__ldcs(&in[(size_t)r * blockDim.x + threadIdx.x]), sm, it);
+      if (threadIdx.x == 0) out[r] = s;
+    }
+    return;
+  }
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 q[P > 0 ? P : 1];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const int r = blockIdx.x + k * gridDim.x;
+    q[k] = r < n_red ? __ldcs(&in[(size_t)r * blockDim.x + threadIdx.x]) : zero;
+  }
   int it = 0;
   for (int r = blockIdx.x; r < n_red; r += gridDim.x, ++it) {
-    const float4 v = __ldcs(&in[(size_t)r * blockDim.x + threadIdx.x]);
+    const float4 v = q[0];
+#pragma unroll
+    for (int k = 0; k + 1 < P; ++k) q[k] = q[k + 1];
+    const int rn = r + P * gridDim.x;
+    q[P - 1] = rn < n_red ? __ldcs(&in[(size_t)rn * blockDim.x + threadIdx.x]) : zero;
     const float4 s = reduce_once<K>(v, sm, it);
     if (threadIdx.x == 0) out[r] = s;
   }
