@@ -30,7 +30,7 @@ def main():
 
     dev = Device(0)
     lib = dev.lib
-    seeds = np.arange(100, dtype=np.uint64) + np.uint64(1_000_000)
+    seeds = np.arange(int(os.environ.get("PHASE_RUNS", "100")), dtype=np.uint64) + np.uint64(1_000_000)
     out = (C.c_uint64 * 16)()
     dev.lga_run_batch(c3(), BASELINE, SINGLE, LgaSettings(), seeds)  # warm
     assert lib.mdr_phase_prof(out, 1) == 0, lib.mdr_last_error(None)
