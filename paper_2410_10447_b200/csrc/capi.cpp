@@ -1238,6 +1238,7 @@ static mdr_lga_batch* lga_batch_alloc(mdr_ctx* ctx, int method, int accum, const
   parts.push_back({(void**)&D.conv, sizeof(int) * Rr});
   parts.push_back({(void**)&D.status, sizeof(int) * Rr});
   parts.push_back({(void**)&D.ls_next, sizeof(int) * (size_t)(D.gens + 1)});
+  parts.push_back({(void**)&D.ls_done, sizeof(int) * Rr});
   parts.push_back({(void**)&b->seeds, sizeof(uint64_t) * Rr});
   for (auto& p : parts) off += al(p.second);
   if (cudaMalloc(&b->block, off) != cudaSuccess || cudaMemset(b->block, 0, off) != cudaSuccess) {

@@ -628,33 +628,6 @@ __global__ void MDR_LS_BOUNDS lga_ls_pair_kernel(LigandView L, LgaDev D) {
   }
 }
 
-// First occurrence of the strict minimum of candidate energies e(0..n-1)
-// (NaN never wins), by the calling warp: the result of applying
-// track_best (docking.cpp:408-413) to the candidates in order, starting from
-// `cur`.  Returns -1 when no candidate is below `cur`.
-template <class E>
-__device__ __forceinline__ int warp_first_min(int n, double cur, E&& energy) {
-  const int lane = threadIdx.x & 31;
-  double m = cur;
-  int idx = -1;
-  for (int k = lane; k < n; k += 32) {
-    const double e = energy(k);
-    if (e < m) {  // per lane, k ascending: first occurrence kept
-      m = e;
-      idx = k;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const double om = __shfl_xor_sync(kFull, m, off);
-    const int oi = __shfl_xor_sync(kFull, idx, off);
-    if (oi >= 0 && (idx < 0 || om < m || (om == m && oi < idx))) {
-      m = om;
-      idx = oi;
-    }
-  }
-  return idx;
-}
 
 // Initial population bookkeeping (docking.cpp:405-422), warp per run:
 // track_best over the P scored individuals in index order.
@@ -674,6 +647,7 @@ __global__ void lga_init_finalize(LgaDev D) {
     D.conv[run] = 0;
     D.status[run] = MDR_OK;
     D.active[run] = D.gens > 0 && budget_ok(D, D.P);
+    D.ls_done[run] = 0;
   }
   if (run == 0)  // work counters of the persistent search kernel: one per generation, one for the polish
     for (int g = lane; g <= D.gens; g += 32) D.ls_next[g] = 0;
@@ -685,47 +659,9 @@ __global__ void lga_init_finalize(LgaDev D) {
 // sequential best tracking is the first occurrence of the minimum over that
 // candidate order; write-backs go to distinct offspring and run in parallel.
 __global__ void lga_gen_finalize(LgaDev D, int gen) {
-  const int lane = threadIdx.x & 31;
   const int run = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (run >= D.R || !D.active[run]) return;
-  const int c = D.cur[run];
-  double* nxt = D.pop[c ^ 1] + (size_t)run * D.P * D.dim;
-  double* ne = D.pope[c ^ 1] + (size_t)run * D.P;
-  const size_t o0 = (size_t)run * D.L;
-  const int n = D.off + D.L;
-  const int w = warp_first_min(n, D.best_e[run], [&](int k) { return k < D.off ? ne[1 + k] : D.lse[o0 + k - D.off]; });
-  if (w >= 0) {  // copy the winner before any write-back overwrites it
-    const double* g = w < D.off ? nxt + (size_t)(1 + w) * D.dim : D.lsg + (o0 + w - D.off) * D.dim;
-    for (int d = lane; d < D.dim; d += 32) D.best_g[(size_t)run * D.dim + d] = g[d];
-    if (lane == 0) D.best_e[run] = w < D.off ? ne[1 + w] : D.lse[o0 + w - D.off];
-  }
-  __syncwarp();
-  long long it = 0;
-  for (int r = lane; r < D.L; r += 32) it += D.lsit[o0 + r] + 1;
-  for (int q = lane; q < D.L * D.dim; q += 32) {
-    const int r = q / D.dim, d = q % D.dim;
-    nxt[(size_t)D.lstarget[o0 + r] * D.dim + d] = D.lsg[(o0 + r) * D.dim + d];
-  }
-  const int k0 = D.nrec[run];
-  for (int r = lane; r < D.L; r += 32) {
-    ne[D.lstarget[o0 + r]] = D.lse[o0 + r];
-    if (k0 + r < D.maxrec) {
-      mdr_ls_record rec;
-      rec.best_energy = D.lse[o0 + r];
-      rec.iterations = D.lsit[o0 + r];
-      rec.converged = D.lscv[o0 + r];
-      D.recs[(size_t)run * D.maxrec + k0 + r] = rec;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) it += __shfl_xor_sync(kFull, it, off);
-  if (lane == 0) {
-    const long long evals = D.evals[run] + D.off + it;
-    D.nrec[run] = k0 + D.L;
-    D.evals[run] = evals;
-    D.cur[run] = c ^ 1;
-    D.active[run] = (gen + 1 < D.gens) && D.status[run] == MDR_OK && budget_ok(D, evals);
-  }
+  gen_finalize_run(D, gen, run);
 }
 
 // Final polish from the incumbent best (docking.cpp:501-515), warp per run.
@@ -1097,15 +1033,16 @@ cudaError_t launch_lga(const LigandView& L, const LgaDev& D, int method, int pai
       if (cta_warps > 0)
         dispatch_lga_ls_cta_kernel(method, pair, D.R * D.L, 32 * cta_warps, cs, s, L, D);
       else if (ls_multi_supported(L, pair, wpb, cta_warps))
-        launch_ls_multi(L, D, method, gen, s);
+        launch_ls_multi(L, D, method, gen, s);  // finalizes each run inside (MDR_LS_FUSE_FINALIZE)
       else if (use_ls_pair(L, pair, wpb, cta_warps))
         launch_ls_pair(method, blocks_for((long long)D.R * D.L, wpb), 64 * wpb, smem, s, L, D);
       else
         dispatch_lga_ls_kernel(method, pair, L, blocks_for((long long)D.R * D.L, wpb), 32 * wpb, smem, s, L, D);
     }
     if (ls_events) cudaEventRecord(ls_events[2 * gen + 1], s);
-    lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
-    launches += D.L > 0 ? 3 : 2;
+    const bool fused = MDR_LS_FUSE_FINALIZE && D.L > 0 && cta_warps == 0 && ls_multi_supported(L, pair, wpb, cta_warps);
+    if (!fused) lga_gen_finalize<<<(D.R + 3) / 4, 128, 0, s>>>(D, gen);
+    launches += (D.L > 0 ? 2 : 1) + (fused ? 0 : 1);
   }
   if (ls_events) cudaEventRecord(ls_events[2 * D.gens], s);
   if (polish_multi(L, pair, wpb, cta_warps)) {

@@ -72,6 +72,9 @@ cudaError_t launch_sincos_selftest(uint64_t seed, long long n, unsigned long lon
 cudaError_t launch_dsqrt_selftest(uint64_t seed, long long n, unsigned long long* mismatches, cudaStream_t s);
 
 // ls_multi.cu: the LGA's Lamarckian search on L.ls_warps warps per search
+#ifndef MDR_LS_FUSE_FINALIZE
+#define MDR_LS_FUSE_FINALIZE 1  // the persistent search's last search of a run does the run's generation bookkeeping
+#endif
 bool ls_multi_supported(const LigandView& L, int pair, int wpb, int cta_warps);
 cudaError_t prep_ls_multi(const LigandView& L, int method);
 void launch_ls_multi(const LigandView& L, const LgaDev& D, int method, int gen, cudaStream_t s);

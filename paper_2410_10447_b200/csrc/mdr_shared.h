@@ -105,6 +105,7 @@ struct LgaDev {
   int* conv;        // [R]
   int* status;      // [R]
   int* ls_next;     // [gens + 1]: next search of generation g / next polish ([gens]) for the persistent search kernel (zeroed at init)
+  int* ls_done;     // [R]: searches of the current generation finished per run (persistent search kernel; the last one finalizes)
 };
 
 }  // namespace mdr
